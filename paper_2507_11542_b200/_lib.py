@@ -1,0 +1,276 @@
+"""ctypes binding of the C ABI in include/lsg.h (liblsg_b200.so).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2507_11542_b200/csrc``).  There is no CPU fallback: if the
+library is missing this module raises on load, and every compute call raises
+``RuntimeError`` when no CUDA device is usable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblsg_b200.so")
+
+# every symbol include/lsg.h declares
+EXPORTS = (
+    "lsg_abi_version", "lsg_last_error", "lsg_opts_default", "lsg_device_count",
+    "lsg_ctx_create", "lsg_nccl_unique_id", "lsg_ctx_create_dist", "lsg_ctx_destroy",
+    "lsg_ctx_synchronize", "lsg_ctx_launch_count",
+    "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis",
+    "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update",
+    "lsg_integrate", "lsg_solve_brt",
+    "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
+    "lsg_solver_set_field", "lsg_solver_get_field", "lsg_solver_set_field_device",
+    "lsg_solver_field_device", "lsg_solver_init_shape", "lsg_solver_step_bound", "lsg_solver_step",
+    "lsg_solver_step_timed",
+    "lsg_solver_integrate", "lsg_solver_stream", "lsg_solver_launches_per_step",
+)
+
+_lib = None
+
+
+def load():
+    """Load liblsg_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the B200 path has no CPU fallback)")
+        lib = C.CDLL(LIB_PATH)
+        lib.lsg_last_error.restype = C.c_char_p
+        lib.lsg_abi_version.restype = C.c_int
+        _lib = lib
+    return _lib
+
+
+def raise_for(rc):
+    if rc == abi.OK:
+        return
+    msg = load().lsg_last_error().decode()
+    if rc == abi.EINVAL:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == abi.ERANGE:
+        raise IndexError(msg)  # std::out_of_range
+    raise RuntimeError(msg)  # std::runtime_error / device faults
+
+
+def call(name, *args):
+    raise_for(getattr(load(), name)(*args))
+
+
+def node_count(g):
+    n = 1
+    for d in range(g.dim):
+        n *= g.counts[d]
+    return n
+
+
+def _steps(log, n, cap):
+    return np.array([[e.t, e.dt, e.step_bound, e.v_min, e.v_max] for e in log[: min(n, cap)]],
+                    dtype=np.float64).reshape(-1, 5)
+
+
+class Context:
+    """One CUDA device + stream (lsg_ctx)."""
+
+    def __init__(self, device=0, rank=0, nranks=1, nccl_id=None):
+        h = C.c_void_p()
+        if nranks > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("distributed context needs the 128-byte NCCL unique id")
+            buf = (C.c_ubyte * 128).from_buffer_copy(bytes(nccl_id))
+            call("lsg_ctx_create_dist", C.c_int(device), C.c_int(rank), C.c_int(nranks), buf, C.byref(h))
+        else:
+            call("lsg_ctx_create", C.c_int(device), C.byref(h))
+        self.h = h
+        self.device, self.rank, self.nranks = device, rank, nranks
+
+    def close(self):
+        if self.h:
+            load().lsg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        call("lsg_ctx_synchronize", self.h)
+
+    def launches(self):
+        n = C.c_uint64()
+        call("lsg_ctx_launch_count", self.h, C.byref(n))
+        return n.value
+
+    # ---- stateless reference-facing calls --------------------------------
+    def pad_ghost(self, g, v, dim, width):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        n = g.counts[dim] if 0 <= dim < g.dim else 1
+        out = np.empty(max(1, node_count(g) // max(n, 1) * (n + 2 * max(width, 0))), dtype=np.float64)
+        call("lsg_pad_ghost", self.h, C.byref(g), abi.dptr(v), C.c_int(dim), C.c_int(width), abi.dptr(out))
+        return out
+
+    def shift_along_dim(self, g, padded, dim, width, offset):
+        padded = np.ascontiguousarray(padded, dtype=np.float64)
+        out = np.empty(node_count(g), dtype=np.float64)
+        call("lsg_shift_along_dim", self.h, C.byref(g), abi.dptr(padded), C.c_int(dim), C.c_int(width),
+             C.c_int(offset), abi.dptr(out))
+        return out
+
+    def upwind(self, g, v, dim, scheme):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        L = np.empty(node_count(g), dtype=np.float64)
+        R = np.empty(node_count(g), dtype=np.float64)
+        call("lsg_upwind", self.h, C.byref(g), abi.dptr(v), C.c_int(dim), C.c_int(scheme), abi.dptr(L),
+             abi.dptr(R))
+        return L, R
+
+    def term_lf(self, g, p, t, v):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty(node_count(g), dtype=np.float64)
+        b = C.c_double()
+        call("lsg_term_lf", self.h, C.byref(g), C.byref(p), C.c_double(t), abi.dptr(v), abi.dptr(out), C.byref(b))
+        return out, b.value
+
+    def restrict_update(self, dvdt, direction):
+        dvdt = np.ascontiguousarray(dvdt, dtype=np.float64)
+        out = np.empty_like(dvdt)
+        call("lsg_restrict_update", self.h, C.c_size_t(dvdt.size), abi.dptr(dvdt), C.c_int(direction),
+             abi.dptr(out))
+        return out
+
+    def integrate(self, g, p, method, t0, tf, v0, opts=None, log_cap=1 << 16):
+        v = np.array(v0, dtype=np.float64, copy=True)
+        log = (abi.LsgStepLog * log_cap)()
+        n = C.c_size_t()
+        tfin = C.c_double()
+        call("lsg_integrate", self.h, C.byref(g), C.byref(p), C.c_int(method), C.c_double(t0), C.c_double(tf),
+             abi.dptr(v), C.byref(opts) if opts is not None else None, log, C.c_size_t(log_cap), C.byref(n),
+             C.byref(tfin))
+        return v, _steps(log, n.value, log_cap), tfin.value
+
+    def solve_brt(self, g, p, v0, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=1 << 16):
+        v0 = np.ascontiguousarray(v0, dtype=np.float64)
+        N = node_count(g)
+        ck = np.empty(max(1, n_checkpoints) * N, dtype=np.float64)
+        times = np.empty(max(1, n_checkpoints), dtype=np.float64)
+        n_out = C.c_int()
+        log = (abi.LsgStepLog * log_cap)()
+        n = C.c_size_t()
+        secs = C.c_double()
+        call("lsg_solve_brt", self.h, C.byref(g), C.byref(p), abi.dptr(v0), C.c_double(tspan[0]),
+             C.c_double(tspan[1]), C.c_int(n_checkpoints), C.c_int(method),
+             C.byref(opts) if opts is not None else None, abi.dptr(ck), abi.dptr(times), C.byref(n_out), log,
+             C.c_size_t(log_cap), C.byref(n), C.byref(secs))
+        k = n_out.value
+        return ck[: k * N].reshape(k, N), times[:k].copy(), _steps(log, n.value, log_cap), secs.value
+
+
+class Solver:
+    """Device-resident value function (lsg_solver): the fast path."""
+
+    def __init__(self, ctx: Context, g, p, method, nslabs=1):
+        self.ctx = ctx
+        self.g, self.p, self.method = g, p, method
+        h = C.c_void_p()
+        if nslabs == 1:
+            call("lsg_solver_create", ctx.h, C.byref(g), C.byref(p), C.c_int(method), C.byref(h))
+        else:
+            call("lsg_solver_create_slabs", ctx.h, C.byref(g), C.byref(p), C.c_int(method), C.c_int(nslabs),
+                 C.byref(h))
+        self.h = h
+        z0, nz, nodes = C.c_int(), C.c_int(), C.c_size_t()
+        call("lsg_solver_slab", h, C.byref(z0), C.byref(nz), C.byref(nodes))
+        self.z0, self.nz, self.local_nodes = z0.value, nz.value, nodes.value
+
+    def close(self):
+        if self.h:
+            load().lsg_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_field(self, v):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.size != self.local_nodes:
+            raise ValueError("field: data size does not match the local node count")
+        call("lsg_solver_set_field", self.h, abi.dptr(v))
+
+    def get_field(self):
+        out = np.empty(self.local_nodes, dtype=np.float64)
+        call("lsg_solver_get_field", self.h, abi.dptr(out))
+        return out
+
+    def set_field_device(self, ptr):
+        call("lsg_solver_set_field_device", self.h, C.c_void_p(ptr))
+
+    def field_device(self):
+        p = C.c_void_p()
+        call("lsg_solver_field_device", self.h, C.byref(p))
+        return p.value
+
+    def init_shape(self, shape, center, radius, ignored_dims=()):
+        mask = 0
+        for d in ignored_dims:
+            mask |= 1 << d
+        c = np.zeros(abi.MAX_DIM, dtype=np.float64)
+        c[: len(center)] = center
+        call("lsg_solver_init_shape", self.h, C.c_int(shape), C.c_uint(mask), abi.dptr(c), C.c_double(radius))
+
+    def step_bound(self, t=0.0):
+        b = C.c_double()
+        call("lsg_solver_step_bound", self.h, C.c_double(t), C.byref(b))
+        return b.value
+
+    def step(self, t, dt):
+        call("lsg_solver_step", self.h, C.c_double(t), C.c_double(dt))
+
+    def step_timed(self, t, dt):
+        """One step with device timing: (per-stage ms list, whole-step ms)."""
+        stage = (C.c_double * 8)()
+        total = C.c_double()
+        call("lsg_solver_step_timed", self.h, C.c_double(t), C.c_double(dt), stage, C.byref(total))
+        return [stage[k] for k in range(self.method + 1)], total.value
+
+    def integrate(self, t0, tf, opts=None, log_cap=1 << 16):
+        log = (abi.LsgStepLog * log_cap)()
+        n = C.c_size_t()
+        tfin = C.c_double()
+        call("lsg_solver_integrate", self.h, C.c_double(t0), C.c_double(tf),
+             C.byref(opts) if opts is not None else None, log, C.c_size_t(log_cap), C.byref(n), C.byref(tfin))
+        return _steps(log, n.value, log_cap), tfin.value
+
+    def stream(self):
+        p = C.c_void_p()
+        call("lsg_solver_stream", self.h, C.byref(p))
+        return p.value
+
+    def launches_per_step(self):
+        n = C.c_int()
+        call("lsg_solver_launches_per_step", self.h, C.byref(n))
+        return n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    call("lsg_nccl_unique_id", buf)
+    return bytes(buf)
+
+
+def device_count():
+    n = C.c_int()
+    call("lsg_device_count", C.byref(n))
+    return n.value

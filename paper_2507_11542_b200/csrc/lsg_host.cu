@@ -1,0 +1,1148 @@
+// lsg_host.cu — host runtime and C ABI of the B200 HJ hot path (include/lsg.h).
+//
+// Owns contexts (device + stream [+ NCCL communicator]), device-resident
+// solvers (value function slabs in HBM, coordinate/trig tables, the global
+// Lax-Friedrichs alpha), the exact step control of the reference integrator
+// and the slab halo exchange.
+//
+// Step control.  The reference's dissipation bound takes (t, grid, dim) and
+// never the value function (hamiltonian.hpp:24-25), and every device kind is
+// time-invariant, so alpha, the CFL bound and therefore the whole dt sequence
+// of a leg are known before any stage runs.  run_cfl below replays the
+// reference loop (integrator.cpp:22-97) on the host to build that schedule,
+// enqueues every stage of the leg back to back with no host synchronisation,
+// and synchronises once at the end of the leg to collect the per-step v range
+// (fused into the last stage of each step) and the error flags.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "lsg_misc.cuh"
+
+using namespace lsg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+#define CUDA_CHECK(x)                                                                         \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess) fail(LSG_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define NCCL_CHECK(x)                                                                           \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) fail(LSG_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LSG_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return LSG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return LSG_EINVAL;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t b) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        if (b == 0) return;
+        const cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            cudaGetLastError();
+            fail(LSG_ENOMEM, "device allocation of " + std::to_string(b) + " bytes failed: " + cudaGetErrorString(e));
+        }
+        bytes = b;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// ---- grid helpers (grid.cpp:9-66) ------------------------------------------
+
+void check_grid(const lsg_grid* g) {
+    if (!g) fail(LSG_EINVAL, "grid: null descriptor");
+    if (g->dim <= 0) fail(LSG_EINVAL, "grid: dimension must be at least 1");
+    if (g->dim > LSG_MAX_DIM) fail(LSG_EINVAL, "grid: at most 6 dimensions are supported");
+    for (int d = 0; d < g->dim; ++d) {
+        if (g->counts[d] < 3) fail(LSG_EINVAL, "grid: counts[" + std::to_string(d) + "] must be >= 3");
+        if (!(g->maxs[d] > g->mins[d]))
+            fail(LSG_EINVAL, "grid: max must exceed min in dimension " + std::to_string(d));
+    }
+    if (g->periodic_mask >> g->dim) fail(LSG_EINVAL, "grid: periodic dimension out of range");
+}
+
+double spacing(const lsg_grid* g, int d) {  // grid.cpp:41
+    return (g->maxs[d] - g->mins[d]) / static_cast<double>(g->counts[d] - 1);
+}
+
+long long node_count(const lsg_grid* g) {
+    long long n = 1;
+    for (int d = 0; d < g->dim; ++d) n *= g->counts[d];
+    return n;
+}
+
+int bc_of(const lsg_grid* g, int d) { return (g->periodic_mask >> d) & 1u ? LSG_BC_PERIODIC : LSG_BC_EXTRAPOLATE; }
+
+int ghost_width(int scheme) {  // spatial_derivatives.cpp:10-18
+    switch (scheme) {
+        case LSG_SCHEME_FIRST: return 1;
+        case LSG_SCHEME_ENO2: return 2;
+        case LSG_SCHEME_ENO3: return 3;
+        case LSG_SCHEME_WENO5: return 3;
+    }
+    fail(LSG_EINVAL, "unknown derivative scheme");
+}
+
+int min_nodes(int scheme) {  // spatial_derivatives.cpp:20-28
+    switch (scheme) {
+        case LSG_SCHEME_FIRST: return 3;
+        case LSG_SCHEME_ENO2: return 5;
+        case LSG_SCHEME_ENO3: return 7;
+        case LSG_SCHEME_WENO5: return 7;
+    }
+    fail(LSG_EINVAL, "unknown derivative scheme");
+}
+
+const char* scheme_name(int scheme) {
+    switch (scheme) {
+        case LSG_SCHEME_FIRST: return "upwind_first_first";
+        case LSG_SCHEME_ENO2: return "upwind_first_eno2";
+        case LSG_SCHEME_ENO3: return "upwind_first_eno3";
+        default: return "upwind_first_weno5";
+    }
+}
+
+LineConst line_const(const lsg_grid* g, int d) {
+    LineConst c;
+    c.dx = spacing(g, d);
+    c.inv_dx = 1.0 / c.dx;
+    c.half_inv = 0.5 * c.inv_dx;
+    c.third_inv = c.inv_dx / 3.0;
+    c.dx2 = c.dx * c.dx;
+    return c;
+}
+
+}  // namespace
+
+// ---- context -----------------------------------------------------------------
+
+struct lsg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    int rank = 0;
+    int nranks = 1;
+    ncclComm_t comm = nullptr;
+    DevBuf scratch[4];  // stateless-call staging
+
+    void note_launch(int n = 1) {
+        launches += static_cast<uint64_t>(n);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) fail(LSG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    }
+    double* staging(int k, size_t bytes) {
+        if (scratch[k].bytes < bytes) scratch[k].alloc(bytes);
+        return scratch[k].as<double>();
+    }
+};
+
+namespace {
+
+void activate(lsg_ctx* ctx) {
+    if (!ctx) fail(LSG_EINVAL, "null context");
+    CUDA_CHECK(cudaSetDevice(ctx->device));
+}
+
+StageFn lookup_stage(int kind, int D, int scheme, int mode) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return stage_lookup_linear(D, scheme, mode);
+        case LSG_HAM_NORMAL: return stage_lookup_normal(D, scheme, mode);
+        case LSG_HAM_ROTATION: return stage_lookup_rotation(D, scheme, mode);
+        case LSG_HAM_ROCKETS: return stage_lookup_rockets(D, scheme, mode);
+        case LSG_HAM_AIR3D: return stage_lookup_air3d(D, scheme, mode);
+        case LSG_HAM_DBLINT4: return stage_lookup_dblint4(D, scheme, mode);
+        case LSG_HAM_DUBINS6: return stage_lookup_dubins6(D, scheme, mode);
+    }
+    return nullptr;
+}
+
+AlphaFn lookup_alpha(int kind) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return alpha_lookup_linear();
+        case LSG_HAM_NORMAL: return alpha_lookup_normal();
+        case LSG_HAM_ROTATION: return alpha_lookup_rotation();
+        case LSG_HAM_ROCKETS: return alpha_lookup_rockets();
+        case LSG_HAM_AIR3D: return alpha_lookup_air3d();
+        case LSG_HAM_DBLINT4: return alpha_lookup_dblint4();
+        case LSG_HAM_DUBINS6: return alpha_lookup_dubins6();
+    }
+    return nullptr;
+}
+
+// Grid dimension each kind requires (0: any); mirrors the reference's
+// rocket_hamiltonian dimension check (reachability.cpp:22-25).
+int kind_dim(int kind) {
+    switch (kind) {
+        case LSG_HAM_ROTATION: return 2;
+        case LSG_HAM_ROCKETS: return 3;
+        case LSG_HAM_AIR3D: return 3;
+        case LSG_HAM_DBLINT4: return 4;
+        case LSG_HAM_DUBINS6: return 6;
+    }
+    return 0;
+}
+
+unsigned trig_dims(int kind) {
+    switch (kind) {
+        case LSG_HAM_ROCKETS: return 1u << 2;
+        case LSG_HAM_AIR3D: return 1u << 2;
+        case LSG_HAM_DUBINS6: return (1u << 2) | (1u << 5);
+    }
+    return 0u;
+}
+
+}  // namespace
+
+// ---- solver --------------------------------------------------------------------
+
+struct Slab {
+    int z0 = 0, nz = 0;
+    long long nodes = 0;
+    DevBuf buf[3];
+    double* f[3] = {nullptr, nullptr, nullptr};  // plane 0 of each buffer
+};
+
+struct lsg_solver {
+    lsg_ctx* ctx = nullptr;
+    lsg_grid g{};
+    lsg_problem p{};
+    int method = LSG_CFL3;
+    int D = 0, W = 0;
+    long long plane = 1;     // nodes per plane of the last axis
+    long long total = 0;     // global node count
+    int P = 1;               // slabs across the whole job
+    int halo_w = 0;          // ghost planes per side (0 when the job has one slab)
+    bool distributed = false;
+    std::vector<Slab> slabs;
+    DevBuf tables;
+    const double* axis[kMaxDim] = {};
+    const double* tcos[kMaxDim] = {};
+    const double* tsin[kMaxDim] = {};
+    LineConst lc[kMaxDim] = {};
+    DevBuf dflags;  // unsigned[2]
+    DevBuf dalpha;  // unsigned long long[8]: D keys, slot 7 = flags
+    DevBuf drange;
+    long long range_cap = 0;
+    long long ring_next = 0;  // ring slot for lsg_solver_step
+    double alpha[kMaxDim] = {};
+    bool alpha_done = false;
+    unsigned alpha_flags = 0;
+    double bound = 0.0;
+    StageFn fn[3] = {nullptr, nullptr, nullptr};
+    std::string invalid;  // deferred invalid_argument (raised at the first term evaluation)
+    int cur = 0;
+};
+
+namespace {
+
+constexpr long long kRingSlots = 4096;
+
+void partition(int n, int P, int r, int* z0, int* nz) {
+    const int base = n / P, rem = n % P;
+    *nz = base + (r < rem ? 1 : 0);
+    *z0 = r * base + std::min(r, rem);
+}
+
+std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int method,
+                                        int nslabs) {
+    activate(ctx);
+    check_grid(g);
+    if (!p) fail(LSG_EINVAL, "term_lax_friedrichs: problem must provide ham_func and dissipation_bounds");
+    if (method < LSG_CFL1 || method > LSG_CFL3) fail(LSG_EINVAL, "unknown integrator");
+    auto s = std::make_unique<lsg_solver>();
+    s->ctx = ctx;
+    s->g = *g;
+    s->p = *p;
+    s->method = method;
+    s->D = g->dim;
+    s->W = ghost_width(p->scheme);
+    s->distributed = ctx->nranks > 1;
+    s->P = s->distributed ? ctx->nranks : nslabs;
+    s->total = node_count(g);
+    for (int d = 0; d + 1 < s->D; ++d) s->plane *= g->counts[d];
+    s->halo_w = s->P > 1 ? s->W : 0;
+    const int nlast = g->counts[s->D - 1];
+    if (s->P > nlast) fail(LSG_EINVAL, "slab decomposition: more slabs than planes along the last axis");
+
+    // kind / dimension / stencil-room checks are deferred to the first term
+    // evaluation, where the reference raises them (reachability.cpp:22,
+    // spatial_derivatives.cpp:40-47).
+    if (lookup_stage(p->kind, 1, 0, 0) == nullptr && lookup_stage(p->kind, s->D, 0, 0) == nullptr &&
+        lookup_alpha(p->kind) == nullptr)
+        s->invalid = "term_lax_friedrichs: problem must provide ham_func and dissipation_bounds";
+    else if (kind_dim(p->kind) && kind_dim(p->kind) != s->D)
+        s->invalid = "hamiltonian: grid dimension does not match the problem kind";
+    for (int d = 0; d < s->D && s->invalid.empty(); ++d)
+        if (g->counts[d] < min_nodes(p->scheme))
+            s->invalid = std::string(scheme_name(p->scheme)) + ": needs at least " +
+                         std::to_string(min_nodes(p->scheme)) + " nodes along dim " + std::to_string(d);
+    if (s->invalid.empty())
+        for (int m = 0; m < 3; ++m) {
+            s->fn[m] = lookup_stage(p->kind, s->D, p->scheme, m);
+            if (!s->fn[m]) s->invalid = "hamiltonian: kind not available for this grid dimension";
+        }
+
+    // slabs
+    const int first = s->distributed ? ctx->rank : 0;
+    const int count = s->distributed ? 1 : s->P;
+    const int nbuf = method == LSG_CFL3 ? 3 : 2;
+    for (int r = first; r < first + count; ++r) {
+        Slab sl;
+        partition(nlast, s->P, r, &sl.z0, &sl.nz);
+        if (s->P > 1 && sl.nz < s->W)
+            fail(LSG_EINVAL, "slab decomposition: each slab needs at least " + std::to_string(s->W) + " planes");
+        sl.nodes = static_cast<long long>(sl.nz) * s->plane;
+        const long long padded = static_cast<long long>(sl.nz + 2 * s->halo_w) * s->plane;
+        for (int b = 0; b < nbuf; ++b) {
+            sl.buf[b].alloc(sizeof(double) * static_cast<size_t>(padded));
+            sl.f[b] = sl.buf[b].as<double>() + static_cast<long long>(s->halo_w) * s->plane;
+        }
+        s->slabs.push_back(std::move(sl));
+    }
+
+    // coordinate tables (grid.cpp:50) and host-libm trig tables
+    std::vector<double> host;
+    std::vector<size_t> ax_off(s->D), c_off(s->D, 0), s_off(s->D, 0);
+    const unsigned tmask = trig_dims(p->kind);
+    for (int d = 0; d < s->D; ++d) {
+        const double dx = spacing(g, d);
+        ax_off[d] = host.size();
+        for (int i = 0; i < g->counts[d]; ++i) host.push_back(g->mins[d] + static_cast<double>(i) * dx);
+    }
+    for (int d = 0; d < s->D; ++d) {
+        if (!(tmask & (1u << d))) continue;
+        c_off[d] = host.size();
+        for (int i = 0; i < g->counts[d]; ++i) host.push_back(std::cos(host[ax_off[d] + i]));
+        s_off[d] = host.size();
+        for (int i = 0; i < g->counts[d]; ++i) host.push_back(std::sin(host[ax_off[d] + i]));
+    }
+    s->tables.alloc(sizeof(double) * host.size());
+    CUDA_CHECK(cudaMemcpy(s->tables.p, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+    const double* base = s->tables.as<double>();
+    for (int d = 0; d < s->D; ++d) {
+        s->axis[d] = base + ax_off[d];
+        if (tmask & (1u << d)) {
+            s->tcos[d] = base + c_off[d];
+            s->tsin[d] = base + s_off[d];
+        }
+        s->lc[d] = line_const(g, d);
+    }
+    s->dflags.alloc(sizeof(unsigned) * 2);
+    s->dalpha.alloc(sizeof(unsigned long long) * 8);
+    CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, s->dflags.bytes, ctx->stream));
+    s->drange.alloc(sizeof(unsigned long long) * 2 * kRingSlots);
+    s->range_cap = kRingSlots;
+    CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, s->drange.bytes, ctx->stream));
+    return s;
+}
+
+void ensure_range(lsg_solver* s, long long nslots) {
+    if (s->range_cap < nslots) {
+        s->drange.alloc(sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots));
+        s->range_cap = nslots;
+    }
+    CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots),
+                               s->ctx->stream));
+    s->ring_next = 0;
+}
+
+// Global Lax-Friedrichs alpha (hamiltonian.cpp:44-56) and the CFL bound (:68-71).
+void ensure_alpha(lsg_solver* s) {
+    if (s->alpha_done) return;
+    if (!s->invalid.empty()) fail(LSG_EINVAL, s->invalid);
+    lsg_ctx* ctx = s->ctx;
+    CUDA_CHECK(cudaMemsetAsync(s->dalpha.p, 0, s->dalpha.bytes, ctx->stream));
+    AlphaFn fn = lookup_alpha(s->p.kind);
+    for (const Slab& sl : s->slabs) {
+        AlphaParams A{};
+        A.n_local = sl.nodes;
+        A.D = s->D;
+        for (int d = 0; d < s->D; ++d) {
+            A.n[d] = d == s->D - 1 ? sl.nz : s->g.counts[d];
+            A.axis[d] = s->axis[d];
+            A.tcos[d] = s->tcos[d];
+            A.tsin[d] = s->tsin[d];
+        }
+        A.z0 = sl.z0;
+        A.trig_dim = s->p.kind == LSG_HAM_ROCKETS || s->p.kind == LSG_HAM_AIR3D ? 2 : -1;
+        std::memcpy(A.hp, s->p.params, sizeof A.hp);
+        A.out = s->dalpha.as<unsigned long long>();
+        A.flags = reinterpret_cast<unsigned*>(s->dalpha.as<unsigned long long>() + 7);
+        void* args[] = {&A};
+        CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3((unsigned)((sl.nodes + 255) / 256)),
+                                    dim3(256), args, 0, ctx->stream));
+        ctx->note_launch();
+    }
+    if (s->distributed)
+        NCCL_CHECK(ncclAllReduce(s->dalpha.p, s->dalpha.p, 8, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    unsigned long long keys[8];
+    CUDA_CHECK(cudaMemcpyAsync(keys, s->dalpha.p, sizeof keys, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    for (int d = 0; d < s->D; ++d) std::memcpy(&s->alpha[d], &keys[d], sizeof(double));
+    s->alpha_flags = static_cast<unsigned>(keys[7]);
+    double speed = 0.0;
+    for (int d = 0; d < s->D; ++d) speed += s->alpha[d] / spacing(&s->g, d);
+    s->bound = speed > 0.0 ? 1.0 / speed : std::numeric_limits<double>::infinity();
+    s->alpha_done = true;
+}
+
+void check_alpha_valid(lsg_solver* s) {
+    ensure_alpha(s);
+    if (s->alpha_flags & FLAG_BOUND_INVALID)
+        fail(LSG_ENUMERIC, "term_lax_friedrichs: dissipation bound must be finite and non-negative");
+}
+
+// Fill the ghost planes of buffer b: from the neighbour slabs (device copies
+// in-process, NCCL send/recv across ranks); ring for a periodic last axis.
+void exchange(lsg_solver* s, int b) {
+    if (s->halo_w == 0) return;
+    lsg_ctx* ctx = s->ctx;
+    const bool periodic = bc_of(&s->g, s->D - 1) == LSG_BC_PERIODIC;
+    const long long w = s->halo_w;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(w * s->plane);
+    if (!s->distributed) {
+        const int P = s->P;
+        for (int r = 0; r < P; ++r) {
+            Slab& me = s->slabs[r];
+            const int lo = r > 0 ? r - 1 : (periodic ? P - 1 : -1);
+            const int hi = r < P - 1 ? r + 1 : (periodic ? 0 : -1);
+            if (lo >= 0) {
+                const Slab& o = s->slabs[lo];
+                CUDA_CHECK(cudaMemcpyAsync(me.f[b] - w * s->plane, o.f[b] + (o.nz - w) * s->plane, bytes,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+            }
+            if (hi >= 0) {
+                const Slab& o = s->slabs[hi];
+                CUDA_CHECK(cudaMemcpyAsync(me.f[b] + me.nz * s->plane, o.f[b], bytes, cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+            }
+        }
+        return;
+    }
+    const int P = ctx->nranks, r = ctx->rank;
+    const int lo = r > 0 ? r - 1 : (periodic ? P - 1 : -1);
+    const int hi = r < P - 1 ? r + 1 : (periodic ? 0 : -1);
+    Slab& me = s->slabs[0];
+    const size_t cnt = static_cast<size_t>(w * s->plane);
+    // Per peer pair the messages match in issue order: every rank first sends
+    // up, then down, and receives from below before from above.
+    NCCL_CHECK(ncclGroupStart());
+    if (hi >= 0) NCCL_CHECK(ncclSend(me.f[b] + (me.nz - w) * s->plane, cnt, ncclFloat64, hi, ctx->comm, ctx->stream));
+    if (lo >= 0) NCCL_CHECK(ncclSend(me.f[b], cnt, ncclFloat64, lo, ctx->comm, ctx->stream));
+    if (lo >= 0) NCCL_CHECK(ncclRecv(me.f[b] - w * s->plane, cnt, ncclFloat64, lo, ctx->comm, ctx->stream));
+    if (hi >= 0) NCCL_CHECK(ncclRecv(me.f[b] + me.nz * s->plane, cnt, ncclFloat64, hi, ctx->comm, ctx->stream));
+    NCCL_CHECK(ncclGroupEnd());
+}
+
+void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range) {
+    lsg_ctx* ctx = s->ctx;
+    const int D = s->D;
+    for (Slab& sl : s->slabs) {
+        StageParams P{};
+        P.u = sl.f[ui];
+        P.v0 = vi >= 0 ? sl.f[vi] : nullptr;
+        P.out = sl.f[oi];
+        P.n_local = sl.nodes;
+        long long st = 1;
+        for (int d = 0; d < D; ++d) {
+            P.n[d] = d == D - 1 ? sl.nz : s->g.counts[d];
+            P.stride[d] = st;
+            st *= P.n[d];
+            P.bc[d] = bc_of(&s->g, d);
+            P.lc[d] = s->lc[d];
+            P.alpha[d] = s->alpha[d];
+            P.axis[d] = s->axis[d];
+            P.tcos[d] = s->tcos[d];
+            P.tsin[d] = s->tsin[d];
+        }
+        P.z0 = sl.z0;
+        P.nz_glob = s->g.counts[D - 1];
+        P.halo = s->halo_w > 0 ? 1 : 0;
+        P.dt = dt;
+        P.c = c;
+        P.restrict_update = s->p.restrict_update;
+        P.direction = s->p.direction;
+        std::memcpy(P.hp, s->p.params, sizeof P.hp);
+        P.flags = s->dflags.as<unsigned>();
+        P.range = range;
+        void* args[] = {&P};
+        CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->fn[mode]),
+                                    dim3((unsigned)((sl.nodes + 255) / 256)), dim3(256), args, 0, ctx->stream));
+        ctx->note_launch();
+    }
+}
+
+// One TVD-RK step (integrator.cpp:58-85); buffers: cur = v, the others scratch.
+// ev (optional) receives stages+1 events: before the step and after each stage.
+void enqueue_step(lsg_solver* s, double dt, unsigned long long* range, cudaEvent_t* ev = nullptr) {
+    const int a = s->cur;
+    cudaStream_t st = s->ctx->stream;
+    auto mark = [&](int k) {
+        if (ev) CUDA_CHECK(cudaEventRecord(ev[k], st));
+    };
+    mark(0);
+    if (s->method == LSG_CFL1) {
+        const int b = 1 - a;
+        exchange(s, a);
+        launch_stage(s, MODE_EULER, a, -1, b, dt, 0.0, range);
+        mark(1);
+        s->cur = b;
+    } else if (s->method == LSG_CFL2) {
+        const int b = 1 - a;
+        exchange(s, a);
+        launch_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
+        mark(1);
+        exchange(s, b);
+        launch_stage(s, MODE_COMBINE, b, a, a, dt, 0.5, range);
+        mark(2);
+    } else {
+        const int b = (a + 1) % 3, c = (a + 2) % 3;
+        exchange(s, a);
+        launch_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
+        mark(1);
+        exchange(s, b);
+        launch_stage(s, MODE_COMBINE, b, a, c, dt, 0.25, nullptr);
+        mark(2);
+        exchange(s, c);
+        launch_stage(s, MODE_COMBINE, c, a, a, dt, 2.0 / 3.0, range);
+        mark(3);
+    }
+}
+
+int stages_of(int method) { return method + 1; }
+
+void check_options(const lsg_opts* o) {  // integrator.cpp:11-20
+    if (!(o->cfl_factor > 0.0)) fail(LSG_EINVAL, "integrator: cfl_factor must be positive");
+    if (!(o->max_step > 0.0)) fail(LSG_EINVAL, "integrator: max_step must be positive");
+    if (!(o->termination_epsilon > 0.0)) fail(LSG_EINVAL, "integrator: termination_epsilon must be positive");
+    for (size_t k = 1; k < o->n_checkpoint_times; ++k)
+        if (o->checkpoint_times[k] < o->checkpoint_times[k - 1])
+            fail(LSG_EINVAL, "integrator: checkpoint_times must be ascending");
+}
+
+lsg_opts default_opts() {
+    lsg_opts o;
+    o.cfl_factor = 0.32;
+    o.max_step = std::numeric_limits<double>::infinity();
+    o.termination_epsilon = 1e-6;
+    o.checkpoint_times = nullptr;
+    o.n_checkpoint_times = 0;
+    return o;
+}
+
+double smin(double a, double b) { return (b < a) ? b : a; }  // std::min
+
+// run_cfl (integrator.cpp:22-97) over the device-resident field.
+void run_cfl(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in, std::vector<lsg_steplog>& log,
+             double* t_final) {
+    const lsg_opts o = opts_in ? *opts_in : default_opts();
+    check_options(&o);
+    if (!std::isfinite(t0) || !std::isfinite(tf)) fail(LSG_EINVAL, "integrator: tspan must be finite");
+    if (tf < t0) fail(LSG_EINVAL, "integrator: tspan must not be decreasing");
+    log.clear();
+    *t_final = t0;
+    if (tf == t0) return;
+    const double eps_stop = o.termination_epsilon * std::abs(tf);
+    double t = t0;
+    if (!(tf - t > 0.0 && tf - t >= eps_stop)) return;
+    check_alpha_valid(s);  // the first term evaluation validates the bounds
+
+    // the dt schedule of the leg (alpha and the bound are v-independent)
+    bool collapsed = false;
+    while (tf - t > 0.0 && tf - t >= eps_stop) {
+        double target = tf;
+        if (o.n_checkpoint_times) {
+            const double* b = o.checkpoint_times;
+            const double* e = b + o.n_checkpoint_times;
+            const double* next = std::upper_bound(b, e, t);
+            if (next != e && *next < tf) target = *next;
+        }
+        const double remaining = target - t;
+        double dt = smin(remaining, o.max_step);
+        dt = smin(dt, o.cfl_factor * s->bound);
+        if (!(dt > 0.0)) {
+            collapsed = true;
+            break;
+        }
+        const bool lands = dt == remaining;
+        log.push_back({t, dt, s->bound, 0.0, 0.0});
+        t = lands ? target : t + dt;
+    }
+    const long long nsteps = static_cast<long long>(log.size());
+    lsg_ctx* ctx = s->ctx;
+    CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
+    ensure_range(s, std::max<long long>(nsteps, 1));
+    for (long long k = 0; k < nsteps; ++k) enqueue_step(s, log[k].dt, s->drange.as<unsigned long long>() + 2 * k);
+    unsigned flags = 0;
+    if (s->distributed) {
+        NCCL_CHECK(ncclAllReduce(s->dflags.p, s->dflags.p, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
+        if (nsteps)  // both slots are max-reduced: {~min key, max key} per step
+            NCCL_CHECK(ncclAllReduce(s->drange.p, s->drange.p, static_cast<size_t>(2 * nsteps), ncclUint64, ncclMax,
+                                     ctx->comm, ctx->stream));
+    }
+    std::vector<unsigned long long> keys(static_cast<size_t>(2 * nsteps));
+    CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    if (nsteps)
+        CUDA_CHECK(cudaMemcpyAsync(keys.data(), s->drange.p, sizeof(unsigned long long) * keys.size(),
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (flags & FLAG_HAM_NONFINITE)
+        fail(LSG_ENUMERIC, "term_lax_friedrichs: hamiltonian produced a non-finite value");
+    if (collapsed) fail(LSG_ENUMERIC, "integrator: step size collapsed to zero");
+    for (long long k = 0; k < nsteps; ++k) {
+        log[k].v_min = key_to_double(~keys[2 * k]);
+        log[k].v_max = key_to_double(keys[2 * k + 1]);
+    }
+    *t_final = t;
+}
+
+void copy_log(const std::vector<lsg_steplog>& log, lsg_steplog* out, size_t cap, size_t* n) {
+    if (n) *n = log.size();
+    if (out)
+        for (size_t k = 0; k < log.size() && k < cap; ++k) out[k] = log[k];
+}
+
+void upload(lsg_solver* s, const double* host, int b) {
+    lsg_ctx* ctx = s->ctx;
+    if (s->distributed) {
+        const Slab& sl = s->slabs[0];
+        CUDA_CHECK(cudaMemcpyAsync(sl.f[b], host, sizeof(double) * sl.nodes, cudaMemcpyHostToDevice, ctx->stream));
+        return;
+    }
+    for (const Slab& sl : s->slabs)
+        CUDA_CHECK(cudaMemcpyAsync(sl.f[b], host + static_cast<long long>(sl.z0) * s->plane,
+                                   sizeof(double) * sl.nodes, cudaMemcpyHostToDevice, ctx->stream));
+}
+
+void download(lsg_solver* s, double* host, int b) {
+    lsg_ctx* ctx = s->ctx;
+    if (s->distributed) {
+        const Slab& sl = s->slabs[0];
+        CUDA_CHECK(cudaMemcpyAsync(host, sl.f[b], sizeof(double) * sl.nodes, cudaMemcpyDeviceToHost, ctx->stream));
+    } else {
+        for (const Slab& sl : s->slabs)
+            CUDA_CHECK(cudaMemcpyAsync(host + static_cast<long long>(sl.z0) * s->plane, sl.f[b],
+                                       sizeof(double) * sl.nodes, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace
+
+// =============================== C ABI ======================================
+
+extern "C" {
+
+int lsg_abi_version(void) { return LSG_ABI_VERSION; }
+
+const char* lsg_last_error(void) { return g_err.c_str(); }
+
+void lsg_opts_default(lsg_opts* o) {
+    if (o) *o = default_opts();
+}
+
+int lsg_device_count(int* count) {
+    return guarded([&] {
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        *count = n;
+    });
+}
+
+int lsg_ctx_create(int device, lsg_ctx** out) {
+    return guarded([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            fail(LSG_ECUDA, "no CUDA device is available (the B200 path has no CPU fallback)");
+        }
+        if (device < 0 || device >= n) fail(LSG_EINVAL, "device index out of range");
+        auto c = std::make_unique<lsg_ctx>();
+        c->device = device;
+        CUDA_CHECK(cudaSetDevice(device));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c.release();
+    });
+}
+
+int lsg_nccl_unique_id(void* out128) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId id;
+        NCCL_CHECK(ncclGetUniqueId(&id));
+        std::memcpy(out128, &id, sizeof id);
+    });
+}
+
+int lsg_ctx_create_dist(int device, int rank, int nranks, const void* nccl_id128, lsg_ctx** out) {
+    return guarded([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(LSG_EINVAL, "invalid rank/nranks");
+        lsg_ctx* c = nullptr;
+        const int rc = lsg_ctx_create(device, &c);
+        if (rc) fail(rc, g_err);
+        std::unique_ptr<lsg_ctx> owner(c);
+        c->rank = rank;
+        c->nranks = nranks;
+        if (nranks > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id128, sizeof id);
+            NCCL_CHECK(ncclCommInitRank(&c->comm, nranks, id, rank));
+        }
+        *out = owner.release();
+    });
+}
+
+int lsg_ctx_destroy(lsg_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->comm) ncclCommDestroy(ctx->comm);
+        for (auto& b : ctx->scratch) b.alloc(0);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int lsg_ctx_synchronize(lsg_ctx* ctx) {
+    return guarded([&] {
+        activate(ctx);
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lsg_ctx_launch_count(const lsg_ctx* ctx, uint64_t* count) {
+    return guarded([&] {
+        if (!ctx) fail(LSG_EINVAL, "null context");
+        *count = ctx->launches;
+    });
+}
+
+int lsg_grid_check(const lsg_grid* g) {
+    return guarded([&] { check_grid(g); });
+}
+
+int lsg_grid_spacing(const lsg_grid* g, int d, double* dx) {
+    return guarded([&] {
+        check_grid(g);
+        if (d < 0 || d >= g->dim) fail(LSG_EINVAL, "grid: dimension out of range");
+        *dx = spacing(g, d);
+    });
+}
+
+int lsg_grid_node_count(const lsg_grid* g, size_t* n) {
+    return guarded([&] {
+        check_grid(g);
+        *n = static_cast<size_t>(node_count(g));
+    });
+}
+
+int lsg_grid_axis(const lsg_grid* g, int d, double* out) {
+    return guarded([&] {
+        check_grid(g);
+        if (d < 0 || d >= g->dim) fail(LSG_EINVAL, "grid: dimension out of range");
+        const double dx = spacing(g, d);
+        for (int i = 0; i < g->counts[d]; ++i) out[i] = g->mins[d] + static_cast<double>(i) * dx;
+    });
+}
+
+int lsg_pad_ghost(lsg_ctx* ctx, const lsg_grid* g, const double* field, int dim, int width, double* out) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        if (dim < 0 || dim >= g->dim) fail(LSG_EINVAL, "pad_ghost: dimension out of range");
+        if (width < 1) fail(LSG_EINVAL, "pad_ghost: width must be >= 1");
+        const int n = g->counts[dim];
+        if (width >= n) fail(LSG_EINVAL, "pad_ghost: width must be smaller than the node count along dim");
+        const long long N = node_count(g);
+        const long long n_out = N / n * (n + 2 * width);
+        long long stride = 1;
+        for (int d = 0; d < dim; ++d) stride *= g->counts[d];
+        double* du = ctx->staging(0, sizeof(double) * N);
+        double* dout = ctx->staging(1, sizeof(double) * n_out);
+        CUDA_CHECK(cudaMemcpyAsync(du, field, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+        launch_pad(du, dout, n_out, n, stride, width, bc_of(g, dim), ctx->stream);
+        ctx->note_launch();
+        CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * n_out, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lsg_shift_along_dim(lsg_ctx* ctx, const lsg_grid* g, const double* padded, int dim, int width, int offset,
+                        double* out) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        if (dim < 0 || dim >= g->dim) fail(LSG_EINVAL, "shift_along_dim: dimension out of range");
+        if (width < 0) fail(LSG_EINVAL, "shift_along_dim: width must be >= 0");
+        if (offset < -width || offset > width)
+            fail(LSG_EINVAL, "shift_along_dim: |offset| must not exceed the ghost width");
+        const int n = g->counts[dim];
+        const long long N = node_count(g);
+        const long long n_in = N / n * (n + 2 * width);
+        long long stride = 1;
+        for (int d = 0; d < dim; ++d) stride *= g->counts[d];
+        double* din = ctx->staging(0, sizeof(double) * n_in);
+        double* dout = ctx->staging(1, sizeof(double) * N);
+        CUDA_CHECK(cudaMemcpyAsync(din, padded, sizeof(double) * n_in, cudaMemcpyHostToDevice, ctx->stream));
+        launch_shift(din, dout, N, n, stride, width, offset, ctx->stream);
+        ctx->note_launch();
+        CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lsg_upwind(lsg_ctx* ctx, const lsg_grid* g, const double* v, int dim, int scheme, double* left, double* right) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        if (scheme < LSG_SCHEME_FIRST || scheme > LSG_SCHEME_WENO5) fail(LSG_EINVAL, "unknown derivative scheme");
+        const char* name = scheme_name(scheme);
+        if (dim < 0 || dim >= g->dim) fail(LSG_EINVAL, std::string(name) + ": dimension out of range");
+        if (g->counts[dim] < min_nodes(scheme))
+            fail(LSG_EINVAL, std::string(name) + ": needs at least " + std::to_string(min_nodes(scheme)) +
+                                 " nodes along dim " + std::to_string(dim));
+        const long long N = node_count(g);
+        double* du = ctx->staging(0, sizeof(double) * N);
+        double* dl = ctx->staging(1, sizeof(double) * N);
+        double* dr = ctx->staging(2, sizeof(double) * N);
+        CUDA_CHECK(cudaMemcpyAsync(du, v, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+        StageParams P{};
+        P.u = du;
+        P.n_local = N;
+        long long st = 1;
+        for (int d = 0; d < g->dim; ++d) {
+            P.n[d] = g->counts[d];
+            P.stride[d] = st;
+            st *= g->counts[d];
+            P.bc[d] = bc_of(g, d);
+            P.lc[d] = line_const(g, d);
+        }
+        launch_upwind(P, dim, g->dim, scheme, dl, dr, ctx->stream);
+        ctx->note_launch();
+        CUDA_CHECK(cudaMemcpyAsync(left, dl, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(right, dr, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t, const double* v, double* dvdt,
+                double* step_bound) {
+    (void)t;
+    return guarded([&] {
+        auto s = make_solver(ctx, g, p, LSG_CFL1, 1);
+        if (!s->invalid.empty()) fail(LSG_EINVAL, s->invalid);
+        upload(s.get(), v, 0);
+        ensure_alpha(s.get());
+        CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
+        launch_stage(s.get(), MODE_TERM, 0, -1, 1, 0.0, 0.0, nullptr);
+        unsigned flags = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof flags, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        // hamiltonian.cpp:37-56: H is validated before the bounds
+        if (flags & FLAG_HAM_NONFINITE)
+            fail(LSG_ENUMERIC, "term_lax_friedrichs: hamiltonian produced a non-finite value");
+        check_alpha_valid(s.get());
+        download(s.get(), dvdt, 1);
+        *step_bound = s->bound;
+    });
+}
+
+int lsg_restrict_update(lsg_ctx* ctx, size_t n, const double* dvdt, int direction, double* out) {
+    return guarded([&] {
+        activate(ctx);
+        if (n == 0) return;
+        double* din = ctx->staging(0, sizeof(double) * n);
+        double* dout = ctx->staging(1, sizeof(double) * n);
+        CUDA_CHECK(cudaMemcpyAsync(din, dvdt, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        launch_restrict(din, dout, static_cast<long long>(n), direction, ctx->stream);
+        ctx->note_launch();
+        CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lsg_integrate(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int method, double t0, double tf, double* v,
+                  const lsg_opts* opts, lsg_steplog* steps, size_t log_cap, size_t* n_steps, double* t_final) {
+    return guarded([&] {
+        if (opts) check_options(opts);
+        auto s = make_solver(ctx, g, p, method, 1);
+        upload(s.get(), v, 0);
+        std::vector<lsg_steplog> log;
+        double tfin = t0;
+        run_cfl(s.get(), t0, tf, opts, log, &tfin);
+        download(s.get(), v, s->cur);
+        copy_log(log, steps, log_cap, n_steps);
+        if (t_final) *t_final = tfin;
+    });
+}
+
+int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const double* v0, double t_first,
+                  double t_second, int n_checkpoints, int method, const lsg_opts* opts, double* checkpoints,
+                  double* checkpoint_times, int* n_out, lsg_steplog* steps, size_t log_cap, size_t* n_steps,
+                  double* integration_seconds) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        // reachability.cpp:138-143
+        if (n_checkpoints < 1) fail(LSG_EINVAL, "solve_brt: need at least one checkpoint");
+        if (!std::isfinite(t_first) || !std::isfinite(t_second)) fail(LSG_EINVAL, "solve_brt: tspan must be finite");
+        const long long N = node_count(g);
+        const double duration = std::abs(t_second - t_first);
+        std::memcpy(checkpoints, v0, sizeof(double) * N);
+        checkpoint_times[0] = 0.0;
+        *n_out = 1;
+        if (n_steps) *n_steps = 0;
+        if (integration_seconds) *integration_seconds = 0.0;
+        if (duration == 0.0 || n_checkpoints == 1) return;
+        auto s = make_solver(ctx, g, p, method, 1);
+        upload(s.get(), v0, 0);
+        const int segments = n_checkpoints - 1;
+        std::vector<lsg_steplog> all, leg;
+        const auto start = std::chrono::steady_clock::now();
+        double t = 0.0;
+        for (int k = 1; k <= segments; ++k) {
+            const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
+            double leg_t = t;
+            run_cfl(s.get(), t, t_end, opts, leg, &leg_t);
+            t = leg_t;
+            all.insert(all.end(), leg.begin(), leg.end());
+            download(s.get(), checkpoints + static_cast<long long>(k) * N, s->cur);
+            checkpoint_times[k] = t_end;
+            *n_out = k + 1;
+        }
+        const auto stop = std::chrono::steady_clock::now();
+        if (integration_seconds) *integration_seconds = std::chrono::duration<double>(stop - start).count();
+        copy_log(all, steps, log_cap, n_steps);
+    });
+}
+
+// ---- device-resident solver ----------------------------------------------
+
+int lsg_solver_create(lsg_ctx* ctx, const lsg_grid* global_grid, const lsg_problem* p, int method,
+                      lsg_solver** out) {
+    return guarded([&] { *out = make_solver(ctx, global_grid, p, method, 1).release(); });
+}
+
+int lsg_solver_create_slabs(lsg_ctx* ctx, const lsg_grid* global_grid, const lsg_problem* p, int method, int nslabs,
+                            lsg_solver** out) {
+    return guarded([&] {
+        if (!ctx) fail(LSG_EINVAL, "null context");
+        if (ctx->nranks > 1) fail(LSG_EINVAL, "in-process slabs need a single-rank context");
+        if (nslabs < 1) fail(LSG_EINVAL, "nslabs must be >= 1");
+        *out = make_solver(ctx, global_grid, p, method, nslabs).release();
+    });
+}
+
+int lsg_solver_destroy(lsg_solver* s) {
+    return guarded([&] {
+        if (!s) return;
+        cudaSetDevice(s->ctx->device);
+        cudaStreamSynchronize(s->ctx->stream);
+        delete s;
+    });
+}
+
+int lsg_solver_slab(const lsg_solver* s, int* z0, int* nz, size_t* local_nodes) {
+    return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (s->distributed) {
+            *z0 = s->slabs[0].z0;
+            *nz = s->slabs[0].nz;
+            *local_nodes = static_cast<size_t>(s->slabs[0].nodes);
+        } else {
+            *z0 = 0;
+            *nz = s->g.counts[s->D - 1];
+            *local_nodes = static_cast<size_t>(s->total);
+        }
+    });
+}
+
+int lsg_solver_set_field(lsg_solver* s, const double* host_v) {
+    return guarded([&] {
+        activate(s->ctx);
+        s->cur = 0;
+        upload(s, host_v, 0);
+        CUDA_CHECK(cudaStreamSynchronize(s->ctx->stream));
+    });
+}
+
+int lsg_solver_get_field(lsg_solver* s, double* host_v) {
+    return guarded([&] {
+        activate(s->ctx);
+        download(s, host_v, s->cur);
+    });
+}
+
+int lsg_solver_set_field_device(lsg_solver* s, const double* dev_v) {
+    return guarded([&] {
+        activate(s->ctx);
+        s->cur = 0;
+        for (const Slab& sl : s->slabs) {
+            const long long off = s->distributed ? 0 : static_cast<long long>(sl.z0) * s->plane;
+            CUDA_CHECK(cudaMemcpyAsync(sl.f[0], dev_v + off, sizeof(double) * sl.nodes, cudaMemcpyDeviceToDevice,
+                                       s->ctx->stream));
+        }
+    });
+}
+
+int lsg_solver_field_device(lsg_solver* s, double** dev_v) {
+    return guarded([&] {
+        if (s->slabs.size() != 1) fail(LSG_EINVAL, "field_device: solver holds several slabs");
+        *dev_v = s->slabs[0].f[s->cur];
+    });
+}
+
+int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const double* center, double radius) {
+    return guarded([&] {
+        activate(s->ctx);
+        if (shape < 0 || shape > 2) fail(LSG_EINVAL, "init_shape: unknown shape");
+        if (!(radius > 0.0)) fail(LSG_EINVAL, "init_shape: radius must be positive");
+        if (shape == 2 && s->D != 6) fail(LSG_EINVAL, "init_shape: pair distance needs a 6-D grid");
+        if (shape == 1) {
+            if (ignored_mask == 0) fail(LSG_EINVAL, "cylinder: ignored_dims must be nonempty");
+            if (ignored_mask >> s->D) fail(LSG_EINVAL, "cylinder: ignored dimension out of range");
+            if (__builtin_popcount(ignored_mask) >= s->D)
+                fail(LSG_EINVAL, "cylinder: at least one dimension must remain active");
+        }
+        s->cur = 0;
+        for (Slab& sl : s->slabs) {
+            ShapeParams S{};
+            S.n_local = sl.nodes;
+            S.D = s->D;
+            for (int d = 0; d < s->D; ++d) {
+                S.n[d] = d == s->D - 1 ? sl.nz : s->g.counts[d];
+                S.axis[d] = s->axis[d];
+                S.center[d] = center ? center[d] : 0.0;
+            }
+            S.z0 = sl.z0;
+            S.shape = shape;
+            S.ignored_mask = shape == 0 ? 0u : ignored_mask;
+            S.radius = radius;
+            S.out = sl.f[0];
+            launch_shape(S, s->ctx->stream);
+            s->ctx->note_launch();
+        }
+    });
+}
+
+int lsg_solver_step_bound(lsg_solver* s, double t, double* bound) {
+    (void)t;
+    return guarded([&] {
+        activate(s->ctx);
+        check_alpha_valid(s);
+        *bound = s->bound;
+    });
+}
+
+int lsg_solver_step(lsg_solver* s, double t, double dt) {
+    (void)t;
+    return guarded([&] {
+        check_alpha_valid(s);
+        if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
+        enqueue_step(s, dt, s->drange.as<unsigned long long>() + 2 * s->ring_next);
+        ++s->ring_next;
+    });
+}
+
+int lsg_solver_step_timed(lsg_solver* s, double t, double dt, double* stage_ms, double* step_ms) {
+    (void)t;
+    return guarded([&] {
+        activate(s->ctx);
+        check_alpha_valid(s);
+        if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
+        const int n = stages_of(s->method);
+        cudaEvent_t ev[4];
+        for (int k = 0; k <= n; ++k) CUDA_CHECK(cudaEventCreate(&ev[k]));
+        enqueue_step(s, dt, s->drange.as<unsigned long long>() + 2 * s->ring_next, ev);
+        ++s->ring_next;
+        CUDA_CHECK(cudaEventSynchronize(ev[n]));
+        for (int k = 0; k < n; ++k) {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+            stage_ms[k] = ms;
+        }
+        float total = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&total, ev[0], ev[n]));
+        *step_ms = total;
+        for (int k = 0; k <= n; ++k) cudaEventDestroy(ev[k]);
+    });
+}
+
+int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* opts, lsg_steplog* steps,
+                         size_t log_cap, size_t* n_steps, double* t_final) {
+    return guarded([&] {
+        activate(s->ctx);
+        std::vector<lsg_steplog> log;
+        double tfin = t0;
+        run_cfl(s, t0, tf, opts, log, &tfin);
+        copy_log(log, steps, log_cap, n_steps);
+        if (t_final) *t_final = tfin;
+    });
+}
+
+int lsg_solver_stream(lsg_solver* s, void** stream) {
+    return guarded([&] { *stream = reinterpret_cast<void*>(s->ctx->stream); });
+}
+
+int lsg_solver_launches_per_step(const lsg_solver* s, int* n) {
+    return guarded([&] { *n = stages_of(s->method) * static_cast<int>(s->slabs.size()); });
+}
+
+}  // extern "C"

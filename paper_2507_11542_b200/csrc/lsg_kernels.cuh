@@ -1,0 +1,178 @@
+// lsg_kernels.cuh — kernel templates of the HJ hot path.
+//
+//   stage_kernel   fused ghost fill + upwind L/R per dimension + central costate +
+//                  Hamiltonian + global-LF dissipation + clamp + TVD-RK stage
+//                  combination (+ v range for the step log); nothing but the
+//                  stage output is written to HBM.  Replaces the reference's
+//                  ~3D+4 full-field passes per term (hamiltonian.cpp:11-76) and
+//                  the RK loops (integrator.cpp:58-92).
+//   alpha_kernel   per-dimension max of the dissipation bound: warp shuffle ->
+//                  block (smem) -> one 64-bit atomicMax per block on the bit
+//                  pattern of the non-negative double (exact, order-free).
+//
+// Generic over the grid dimension D (1..6): one thread per node, the
+// cross-shaped stencil read through the read-only data path (neighbouring
+// threads share lines through L1/L2).  Specialised tiled kernels for the
+// benchmark shapes live in lsg_tiled.cuh.
+#pragma once
+
+#include "lsg_device.cuh"
+
+namespace lsg {
+
+using StageFn = void (*)(StageParams);
+
+template <int D, int S, int KIND, int MODE>
+__global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ StageParams P) {
+    constexpr int W = SchemeWidth<S>::W;
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    bool bad = false;
+    if (idx < P.n_local) {
+        int i[D], ix[D];
+        double x[D];
+        long long r = idx;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            if (d == D - 1) {
+                i[d] = (int)r;
+            } else {
+                const long long q = r / P.n[d];
+                i[d] = (int)(r - q * P.n[d]);
+                r = q;
+            }
+            ix[d] = (d == D - 1) ? P.z0 + i[d] : i[d];
+            x[d] = __ldg(P.axis[d] + ix[d]);
+        }
+        double p[D];
+        double diss = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            double s[2 * W + 1];
+            gather_window<W>(P.u, idx, i[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s);
+            double L, R;
+            line_lr<S>(s, P.lc[d], L, R);
+            p[d] = 0.5 * (L + R);              // hamiltonian.cpp:31-32
+            diss += P.alpha[d] * (R - L);       // hamiltonian.cpp:60-64
+        }
+        const double H = hamiltonian<KIND, D>(P, x, ix, p);
+        bad = !isfinite(H);                     // hamiltonian.cpp:38-40
+        double dv = -(H - 0.5 * diss);          // hamiltonian.cpp:65
+        if (P.restrict_update)                  // hamiltonian.cpp:78-88
+            dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
+        double o;
+        if constexpr (MODE == MODE_TERM) {
+            o = dv;
+        } else if constexpr (MODE == MODE_EULER) {
+            o = __ldg(P.u + idx) + P.dt * dv;
+        } else {
+            const double base = P.v0[idx];  // plain load: out may alias v0 (in-place RK update)
+            o = base + P.c * ((__ldg(P.u + idx) + P.dt * dv) - base);
+        }
+        P.out[idx] = o;
+        kmin = kmax = order_key(o);
+    }
+    if (P.flags) {
+        if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
+    }
+    if (P.range) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+        }
+        __shared__ unsigned long long smin[8], smax[8];
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) {
+            smin[warp] = kmin;
+            smax[warp] = kmax;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int nw = blockDim.x >> 5;
+            kmin = lane < nw ? smin[lane] : ~0ull;
+            kmax = lane < nw ? smax[lane] : 0ull;
+#pragma unroll
+            for (int off = 4; off > 0; off >>= 1) {
+                kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+                kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+            }
+            if (lane == 0) {
+                if (kmin != ~0ull) atomicMax(P.range, ~kmin);  // slot 0 holds ~(min key)
+                if (kmax != 0ull) atomicMax(P.range + 1, kmax);
+            }
+        }
+    }
+}
+
+// Parameters of the alpha reduction.
+struct AlphaParams {
+    long long n_local;
+    int D;
+    int n[kMaxDim];
+    int z0;
+    const double* axis[kMaxDim];
+    const double* tcos[kMaxDim];
+    const double* tsin[kMaxDim];
+    int trig_dim;  // axis whose cos/sin the bound uses (-1: none)
+    double hp[LSG_MAX_PARAMS];
+    unsigned long long* out;  // D keys (bit patterns of non-negative doubles)
+    unsigned* flags;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(256) alpha_kernel(const __grid_constant__ AlphaParams A) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double x[kMaxDim] = {0, 0, 0, 0, 0, 0};
+    double ct = 0.0, sn = 0.0;
+    const bool live = idx < A.n_local;
+    if (live) {
+        long long r = idx;
+        for (int d = 0; d < A.D; ++d) {
+            int id;
+            if (d == A.D - 1) {
+                id = (int)r + A.z0;
+            } else {
+                const long long q = r / A.n[d];
+                id = (int)(r - q * A.n[d]);
+                r = q;
+            }
+            x[d] = A.axis[d][id];
+            if (d == A.trig_dim) {
+                ct = A.tcos[d][id];
+                sn = A.tsin[d][id];
+            }
+        }
+    }
+    __shared__ unsigned long long sm[kMaxDim][8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    bool bad = false;
+    for (int d = 0; d < A.D; ++d) {
+        unsigned long long key = 0ull;
+        if (live) {
+            double b = dissipation_bound<KIND>(A.hp, d, x, ct, sn);
+            if (!isfinite(b) || b < 0.0) {  // hamiltonian.cpp:49-53
+                bad = true;
+                b = 0.0;
+            }
+            if (b == 0.0) b = 0.0;  // -0.0 -> +0.0: std::max(0.0, -0.0) keeps +0.0
+            key = (unsigned long long)__double_as_longlong(b);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, off));
+        if (lane == 0) sm[d][warp] = key;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(A.flags, FLAG_BOUND_INVALID);
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        for (int d = 0; d < A.D; ++d) {
+            unsigned long long key = lane < nw ? sm[d][lane] : 0ull;
+#pragma unroll
+            for (int off = 4; off > 0; off >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, off));
+            if (lane == 0 && key) atomicMax(A.out + d, key);
+        }
+    }
+}
+
+}  // namespace lsg

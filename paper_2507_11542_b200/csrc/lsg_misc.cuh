@@ -1,0 +1,49 @@
+// lsg_misc.cuh — host-visible launchers and lookup tables of the device kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lsg_kernels.cuh"
+
+namespace lsg {
+
+struct ShapeParams {
+    long long n_local;
+    int D;
+    int n[kMaxDim];
+    int z0;
+    const double* axis[kMaxDim];
+    int shape;
+    unsigned ignored_mask;
+    double center[kMaxDim];
+    double radius;
+    double* out;
+};
+
+using AlphaFn = void (*)(AlphaParams);
+
+StageFn stage_lookup_linear(int D, int s, int m);
+StageFn stage_lookup_normal(int D, int s, int m);
+StageFn stage_lookup_rotation(int D, int s, int m);
+StageFn stage_lookup_rockets(int D, int s, int m);
+StageFn stage_lookup_air3d(int D, int s, int m);
+StageFn stage_lookup_dblint4(int D, int s, int m);
+StageFn stage_lookup_dubins6(int D, int s, int m);
+AlphaFn alpha_lookup_linear();
+AlphaFn alpha_lookup_normal();
+AlphaFn alpha_lookup_rotation();
+AlphaFn alpha_lookup_rockets();
+AlphaFn alpha_lookup_air3d();
+AlphaFn alpha_lookup_dblint4();
+AlphaFn alpha_lookup_dubins6();
+
+void launch_upwind(const StageParams& P, int dim, int D, int scheme, double* left, double* right, cudaStream_t st);
+void launch_pad(const double* u, double* out, long long n_out, int n, long long stride, int width, int bc,
+                cudaStream_t st);
+void launch_shift(const double* padded, double* out, long long N, int n, long long stride, int width, int offset,
+                  cudaStream_t st);
+void launch_restrict(const double* in, double* out, long long n, int direction, cudaStream_t st);
+void launch_shape(const ShapeParams& S, cudaStream_t st);
+void launch_range_init(unsigned long long* r, long long nslots, cudaStream_t st);
+
+}  // namespace lsg

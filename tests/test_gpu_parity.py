@@ -1,0 +1,290 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle.
+
+Bit-exact for the ENO/First schemes, step bounds, dt sequences and step
+counts, and — because the WENO5 kernel keeps the reference's operation order
+with IEEE divisions — for WENO5 as well.  The north_star tolerance (1e-10
+relative in fp64) is the fallback bar asserted where noted.
+"""
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import assert_bitwise, rel_inf
+from paper_2507_11542_b200 import _lib, abi
+from paper_2507_11542_b200 import problems as P
+import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(os.path.join(GOLDEN, "golden.npz"))
+
+
+@pytest.fixture(scope="module")
+def sums():
+    with open(os.path.join(GOLDEN, "golden_sums.json")) as f:
+        return json.load(f)
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def test_pad_and_shift_vs_golden(ctx, golden):
+    g = abi.make_grid([0.0] * 3, [1.0] * 3, [5, 6, 7], [0, 1, 2])
+    v = golden["pad/periodic/in"]
+    for d in range(3):
+        p = ctx.pad_ghost(g, v, d, 2)
+        assert_bitwise(p, golden[f"pad/periodic/d{d}"], f"pad periodic d{d}")
+        for off in (-2, -1, 0, 1, 2):
+            back = ctx.shift_along_dim(g, ctx.pad_ghost(g, ctx.shift_along_dim(g, p, d, 2, off), d, 2), d, 2, -off)
+            assert_bitwise(back, v, "shift round trip")
+    g = abi.make_grid([0.0] * 3, [1.0] * 3, [5, 6, 7])
+    for d in range(3):
+        assert_bitwise(ctx.pad_ghost(g, golden["pad/extrap/in"], d, 3), golden[f"pad/extrap/d{d}"], f"pad extrap d{d}")
+    with pytest.raises(ValueError):
+        ctx.pad_ghost(abi.make_grid([0.0], [1.0], [4]), np.zeros(4), 0, 4)
+
+
+@pytest.mark.parametrize("key", ["A", "B", "C"])
+def test_upwind_vs_golden(ctx, golden, key):
+    from golden.make_golden import UPWIND_GRIDS
+
+    g, _ = UPWIND_GRIDS[key]
+    v = golden[f"upwind/{key}/in"]
+    for s in range(4):
+        for d in range(g.dim):
+            L, R = ctx.upwind(g, v, d, s)
+            assert_bitwise(L, golden[f"upwind/{key}/s{s}/d{d}/L"], f"{key} s{s} d{d} L")
+            assert_bitwise(R, golden[f"upwind/{key}/s{s}/d{d}/R"], f"{key} s{s} d{d} R")
+
+
+@pytest.mark.parametrize("dims", [(7,), (9, 8), (8, 7, 9), (7, 7, 7, 8), (7, 7, 7, 7, 7), (7,) * 6])
+def test_upwind_vs_oracle_all_dims(ctx, port, dims):
+    D = len(dims)
+    for periodic in [(), tuple(range(D))]:
+        g = abi.make_grid([-1.0] * D, [1.5] * D, list(dims), periodic)
+        v = H.random_field(g, 11 + D)
+        for s in range(4):
+            for d in range(D):
+                a, b = ctx.upwind(g, v, d, s), port.upwind(g, v, d, s)
+                assert_bitwise(a[0], b[0], f"D{D} s{s} d{d} L")
+                assert_bitwise(a[1], b[1], f"D{D} s{s} d{d} R")
+
+
+def test_upwind_errors(ctx):
+    g = abi.make_grid([0.0], [1.0], [5])
+    ctx.upwind(g, np.zeros(5), 0, abi.SCHEME_ENO2)
+    for s, dim in [(abi.SCHEME_ENO3, 0), (abi.SCHEME_WENO5, 0), (abi.SCHEME_FIRST, 1)]:
+        with pytest.raises(ValueError):
+            ctx.upwind(g, np.zeros(5), dim, s)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "rockets", "rotation"])
+def test_term_vs_golden(ctx, port, sums, name):
+    S = P.CONFIGS[name](**H.small(name))
+    v0 = H.initial_value(port, S)
+    dvdt, bound = ctx.term_lf(S.grid, S.problem, 0.0, v0)
+    e = sums[f"term/{name}"]
+    assert bound.hex() == e["bound"], "step bound must be bit-exact"
+    if sha(dvdt) != e["dvdt"]:
+        ref_dvdt, _ = port.term_lf(S.grid, S.problem, 0.0, v0)
+        assert_bitwise(dvdt, ref_dvdt, f"dvdt {name}")
+
+
+@pytest.mark.parametrize("scheme", [0, 1, 2, 3])
+@pytest.mark.parametrize("clamp", [False, True])
+def test_term_linear_all_schemes(ctx, port, scheme, clamp):
+    g = abi.make_grid([0.0, -1.0, 0.0], [1.0, 1.0, 2.0], [12, 9, 10], [2])
+    v = H.random_field(g, 99)
+    p = abi.make_problem(abi.HAM_LINEAR, scheme, abi.linear_params([0.7, -1.3, 0.2]), abi.SHRINK, clamp)
+    a, ba = ctx.term_lf(g, p, 0.0, v)
+    b, bb = port.term_lf(g, p, 0.0, v)
+    assert_bitwise(a, b, "dvdt")
+    assert ba == bb
+
+
+def test_term_kats(ctx):
+    # test_hamiltonian.cpp:54-193 on the device path
+    lin = lambda c, bounds=None, offset=0.0, scheme=abi.SCHEME_ENO2: abi.make_problem(  # noqa: E731
+        abi.HAM_LINEAR, scheme, abi.linear_params(c, bounds, offset))
+    g = abi.make_grid([0.0], [1.0], [11])
+    assert ctx.term_lf(g, lin([2.0]), 0.0, np.zeros(11))[1] == pytest.approx(0.05, rel=1e-14)
+    assert ctx.term_lf(g, lin([0.0]), 0.0, np.zeros(11))[1] == math.inf
+    g = abi.make_grid([0.0], [2.0], [5])
+    x = np.linspace(0.0, 2.0, 5)
+    assert ctx.term_lf(g, lin([1.0], [0.0], scheme=abi.SCHEME_FIRST), 0.0, x * x)[0][2] == pytest.approx(-2.0)
+    g = abi.make_grid([0.0], [1.0], [17])
+    d, _ = ctx.term_lf(g, lin([0.25], [0.25], 0.125), 0.0, 1.5 * np.arange(17) / 16.0)
+    assert np.all(d == -(0.25 * 1.5 + 0.125))
+    g = abi.make_grid([0.0], [1.0], [5])
+    with pytest.raises(RuntimeError):
+        ctx.term_lf(g, lin([math.nan]), 0.0, np.ones(5))
+    with pytest.raises(RuntimeError):
+        ctx.term_lf(g, lin([1.0], [-1.0]), 0.0, np.ones(5))
+    with pytest.raises(RuntimeError):
+        ctx.term_lf(g, lin([1.0], [math.inf]), 0.0, np.ones(5))
+    assert list(ctx.restrict_update(np.array([-2.0, 0.0, 3.0]), abi.GROW)) == [-2.0, 0.0, 0.0]
+    assert list(ctx.restrict_update(np.array([-2.0, 0.0, 3.0]), abi.SHRINK)) == [0.0, 0.0, 3.0]
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "rotation"])
+def test_integrate_vs_oracle(ctx, port, name):
+    S = P.CONFIGS[name](**H.small(name))
+    v0 = H.initial_value(port, S)
+    tf = 0.03
+    va, sa, ta = ctx.integrate(S.grid, S.problem, S.method, 0.0, tf, v0, abi.make_opts())
+    vb, sb, tb = port.integrate(S.grid, S.problem, S.method, 0.0, tf, v0, abi.make_opts())
+    assert ta == tb
+    assert_bitwise(sa, sb, "step log (t, dt, bound, v_min, v_max)")
+    assert_bitwise(va, vb, "final value function")
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg5", "rotation"])
+def test_integrate_vs_golden(ctx, port, sums, name):
+    e = sums[f"integrate/{name}"]
+    S = P.CONFIGS[name](**e["kw"])
+    v0 = H.initial_value(port, S)
+    v, steps, tfin = ctx.integrate(S.grid, S.problem, S.method, 0.0, e["tf"], v0, abi.make_opts())
+    assert len(steps) == e["n_steps"]
+    assert [[x.hex() for x in row] for row in steps] == e["steps"]
+    assert tfin.hex() == e["t_final"]
+    assert sha(v) == e["out"]
+
+
+def test_integrate_methods_and_checkpoints(ctx, port):
+    S = P.cfg2_air3d(15)
+    v0 = H.initial_value(port, S)
+    o = abi.make_opts(checkpoint_times=[0.011, 0.05], max_step=0.02)
+    for m in (abi.CFL1, abi.CFL2, abi.CFL3):
+        a = ctx.integrate(S.grid, S.problem, m, 0.0, 0.07, v0, o)
+        b = port.integrate(S.grid, S.problem, m, 0.0, 0.07, v0, o)
+        assert_bitwise(a[1], b[1], f"steps m{m}")
+        assert_bitwise(a[0], b[0], f"v m{m}")
+        assert 0.011 in a[1][:, 0] and 0.05 in a[1][:, 0]
+
+
+def test_integrate_errors(ctx, port):
+    S = P.cfg1_circle(21)
+    v0 = H.initial_value(port, S)
+    for bad in [abi.make_opts(cfl_factor=0.0), abi.make_opts(max_step=-1.0),
+                abi.make_opts(checkpoint_times=[0.5, 0.2])]:
+        with pytest.raises(ValueError):
+            ctx.integrate(S.grid, S.problem, abi.CFL1, 0.0, 1.0, v0, bad)
+    with pytest.raises(ValueError):
+        ctx.integrate(S.grid, S.problem, abi.CFL1, 1.0, 0.0, v0)
+    v, steps, t = ctx.integrate(S.grid, S.problem, abi.CFL2, 4.0, 4.0, v0)
+    assert t == 4.0 and len(steps) == 0 and np.array_equal(v, v0)
+    nan_p = abi.make_problem(abi.HAM_LINEAR, abi.SCHEME_ENO2, abi.linear_params([math.nan, 1.0], [1.0, 1.0]))
+    with pytest.raises(RuntimeError):
+        ctx.integrate(S.grid, nan_p, abi.CFL3, 0.0, 0.1, v0)
+    # a rockets problem on a 2-D grid is rejected like rocket_hamiltonian does
+    rk = P.rockets(9).problem
+    with pytest.raises(ValueError):
+        ctx.integrate(S.grid, rk, abi.CFL3, 0.0, 0.1, v0)
+
+
+def test_solve_brt_rockets20_vs_golden(ctx, golden):
+    S = P.rockets(20)
+    v0 = golden["brt/rockets20/in"]
+    ck, times, steps, secs = ctx.solve_brt(S.grid, S.problem, v0, (-0.5, 0.0), 3, abi.CFL3, abi.make_opts())
+    assert_bitwise(ck, golden["brt/rockets20/ck"], "checkpoints")
+    assert_bitwise(times, golden["brt/rockets20/times"], "checkpoint times")
+    assert_bitwise(steps, golden["brt/rockets20/steps"], "step log")
+    assert secs > 0
+
+
+def test_solve_brt_rockets50_acceptance(ctx, port, sums):
+    """acceptance.cpp:381-419: rockets N=50, (-2.5, 0), 11 checkpoints -> 490 steps,
+    full step log and final field bit-identical to the reference."""
+    S = P.rockets(50)
+    v0 = H.initial_value(port, S)
+    ck, times, steps, _ = ctx.solve_brt(S.grid, S.problem, v0, (-2.5, 0.0), 11, abi.CFL3, abi.make_opts())
+    e = sums["rockets50"]
+    assert len(steps) == 490
+    assert [[x.hex() for x in row] for row in steps] == e["steps"]
+    assert sha(ck[-1]) == e["out"]
+    assert np.all(np.diff(ck, axis=0) <= 0.0), "the Grow clamp makes checkpoints non-increasing"
+
+
+def test_cfg1_full_size_vs_golden(ctx, port, sums):
+    """BASELINE configs[0] end to end: 101^2 ENO2 + odeCFL2 over (0, 0.5)."""
+    e = sums["integrate/cfg1"]
+    S = P.cfg1_circle(101)
+    v0 = H.initial_value(port, S)
+    v, steps, t = ctx.integrate(S.grid, S.problem, S.method, 0.0, 0.5, v0, abi.make_opts())
+    assert sha(v) == e["out"] and len(steps) == e["n_steps"] == 118
+
+
+@pytest.mark.parametrize("name,nslabs", [("cfg2", 2), ("cfg2", 3), ("cfg5", 4), ("cfg3", 2), ("cfg1", 5),
+                                         ("cfg4", 2)])
+def test_slabs_equal_single_device_bitwise(ctx, port, name, nslabs):
+    """P slabs along the last axis (halo planes exchanged between stages) ==
+    the single-slab result, bit for bit, including the step log."""
+    S = P.CONFIGS[name](**H.small(name))
+    v0 = H.initial_value(port, S)
+    one = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    many = _lib.Solver(ctx, S.grid, S.problem, S.method, nslabs=nslabs)
+    one.set_field(v0)
+    many.set_field(v0)
+    s1, t1 = one.integrate(0.0, 0.04, abi.make_opts())
+    s2, t2 = many.integrate(0.0, 0.04, abi.make_opts())
+    assert t1 == t2
+    assert_bitwise(s1, s2, "step log")
+    assert_bitwise(one.get_field(), many.get_field(), "value function")
+
+
+def test_device_initial_conditions(ctx, port):
+    for name in ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "rockets", "rotation"]:
+        S = P.CONFIGS[name](**H.small(name))
+        s = _lib.Solver(ctx, S.grid, S.problem, S.method)
+        shape, center, radius, ignored = S.ic
+        s.init_shape(shape, center, radius, ignored)
+        assert_bitwise(s.get_field(), H.initial_value(port, S), f"IC {name}")
+
+
+def test_cfg2_full_size_two_steps_vs_oracle(ctx, port):
+    """The bench workload (Air3D 101^3, ENO3 LF + RK3) against the oracle."""
+    S = P.cfg2_air3d(101)
+    v0 = H.initial_value(port, S)
+    solver = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    solver.set_field(v0)
+    tf = 2 * 0.32 * solver.step_bound()
+    sa, ta = solver.integrate(0.0, tf)
+    vb, sb, tb = port.integrate(S.grid, S.problem, S.method, 0.0, tf, v0)
+    assert len(sa) == len(sb) >= 2
+    assert_bitwise(sa, sb, "step log")
+    assert_bitwise(solver.get_field(), vb, "v after 2 steps")
+
+
+def test_cfg5_full_size_properties(ctx):
+    """512^3 periodic WENO5 (1.07 GB per field): translating the initial field by
+    one node along each periodic axis translates the result bit for bit
+    (test_spatial_derivatives.cpp:171-192 lifted to a whole RK3 step), and the
+    4-slab decomposition equals the single-slab run."""
+    S = P.cfg5_normal(512)
+    n = 512
+    base = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    base.init_shape(*S.ic[:3], S.ic[3])
+    v0 = base.get_field()
+    dt = 0.32 * base.step_bound()
+    base.step(0.0, dt)
+    out0 = base.get_field().reshape(n, n, n)
+    moved = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    for axis in range(3):
+        moved.set_field(np.roll(v0.reshape(n, n, n), 1, axis=axis).ravel())
+        moved.step(0.0, dt)
+        assert_bitwise(moved.get_field(), np.roll(out0, 1, axis=axis).ravel(), f"translation axis {axis}")
+    del moved
+    slabs = _lib.Solver(ctx, S.grid, S.problem, S.method, nslabs=4)
+    slabs.set_field(v0)
+    slabs.step(0.0, dt)
+    assert_bitwise(slabs.get_field(), out0.ravel(), "4 slabs vs 1")
