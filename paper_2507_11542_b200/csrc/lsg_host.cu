@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -208,6 +209,21 @@ StageFn lookup_stage(int kind, int D, int scheme, int mode) {
     return nullptr;
 }
 
+March3Fn lookup_march3(int kind, int scheme, int mode) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return march3_lookup_linear(scheme, mode);
+        case LSG_HAM_NORMAL: return march3_lookup_normal(scheme, mode);
+        case LSG_HAM_ROCKETS: return march3_lookup_rockets(scheme, mode);
+        case LSG_HAM_AIR3D: return march3_lookup_air3d(scheme, mode);
+    }
+    return nullptr;
+}
+
+bool force_generic() {
+    const char* e = std::getenv("LSG_KERNEL");
+    return e && std::string(e) == "generic";
+}
+
 AlphaFn lookup_alpha(int kind) {
     switch (kind) {
         case LSG_HAM_LINEAR: return alpha_lookup_linear();
@@ -250,6 +266,8 @@ unsigned trig_dims(int kind) {
 struct Slab {
     int z0 = 0, nz = 0;
     long long nodes = 0;
+    March3 m3{};       // 2.5-D tiling of this slab (3-D grids)
+    dim3 m3_grid;
     DevBuf buf[3];
     double* f[3] = {nullptr, nullptr, nullptr};  // plane 0 of each buffer
 };
@@ -281,6 +299,9 @@ struct lsg_solver {
     unsigned alpha_flags = 0;
     double bound = 0.0;
     StageFn fn[3] = {nullptr, nullptr, nullptr};
+    March3Fn m3fn[3] = {nullptr, nullptr, nullptr};
+    int m3_threads = 0;
+    size_t m3_smem = 0;
     std::string invalid;  // deferred invalid_argument (raised at the first term evaluation)
     int cur = 0;
 };
@@ -334,6 +355,36 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             if (!s->fn[m]) s->invalid = "hamiltonian: kind not available for this grid dimension";
         }
 
+    // 2.5-D tiled kernel for 3-D grids (lsg_march3.cuh)
+    int TX = 0, R = 0;
+    if (s->invalid.empty() && s->D == 3 && !force_generic()) {
+        const int n0 = g->counts[0], n1 = g->counts[1];
+        if (n0 <= 256) {
+            TX = n0;
+            R = std::max(2, 512 / n0);
+        } else {
+            TX = 32;
+            R = 16;
+        }
+        R = std::min(R, n1);
+        const int W = s->W;
+        const int threads = ((TX * R + 31) / 32) * 32;
+        const int halo = 2 * W * TX + (TX < n0 ? 2 * W * R : 0);
+        if (threads <= 512 && halo <= kMaxHalo * threads) {
+            bool all = true;
+            for (int m = 0; m < 3; ++m) {
+                s->m3fn[m] = lookup_march3(p->kind, p->scheme, m);
+                all = all && s->m3fn[m];
+            }
+            if (all) {
+                s->m3_threads = threads;
+                s->m3_smem = sizeof(double) * static_cast<size_t>((TX + 2 * W) * (R + 2 * W));
+            } else {
+                for (auto& f : s->m3fn) f = nullptr;
+            }
+        }
+    }
+
     // slabs
     const int first = s->distributed ? ctx->rank : 0;
     const int count = s->distributed ? 1 : s->P;
@@ -344,6 +395,26 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         if (s->P > 1 && sl.nz < s->W)
             fail(LSG_EINVAL, "slab decomposition: each slab needs at least " + std::to_string(s->W) + " planes");
         sl.nodes = static_cast<long long>(sl.nz) * s->plane;
+        if (s->m3fn[0]) {
+            // tiles x z-chunks: minimise waves * (planes per chunk + warm-up) over 148 SMs
+            const int ntx = (g->counts[0] + TX - 1) / TX, nty = (g->counts[1] + R - 1) / R;
+            const int nt = ntx * nty;
+            double best = 1e300;
+            int best_nzc = 1;
+            for (int nzc = 1; nzc <= sl.nz; ++nzc) {
+                const int chunk = (sl.nz + nzc - 1) / nzc;
+                const int used = (sl.nz + chunk - 1) / chunk;
+                const double waves = std::ceil(static_cast<double>(nt) * used / 148.0);
+                const double cost = waves * (chunk + 0.5 * s->W);
+                if (cost < best - 1e-9) {
+                    best = cost;
+                    best_nzc = used;
+                }
+            }
+            const int chunk = (sl.nz + best_nzc - 1) / best_nzc;
+            sl.m3 = March3{TX, R, ntx, chunk};
+            sl.m3_grid = dim3(static_cast<unsigned>(nt), static_cast<unsigned>((sl.nz + chunk - 1) / chunk));
+        }
         const long long padded = static_cast<long long>(sl.nz + 2 * s->halo_w) * s->plane;
         for (int b = 0; b < nbuf; ++b) {
             sl.buf[b].alloc(sizeof(double) * static_cast<size_t>(padded));
@@ -517,9 +588,15 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
         std::memcpy(P.hp, s->p.params, sizeof P.hp);
         P.flags = s->dflags.as<unsigned>();
         P.range = range;
-        void* args[] = {&P};
-        CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->fn[mode]),
-                                    dim3((unsigned)((sl.nodes + 255) / 256)), dim3(256), args, 0, ctx->stream));
+        if (s->m3fn[mode]) {
+            void* args[] = {&P, &sl.m3};
+            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->m3fn[mode]), sl.m3_grid,
+                                        dim3(static_cast<unsigned>(s->m3_threads)), args, s->m3_smem, ctx->stream));
+        } else {
+            void* args[] = {&P};
+            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->fn[mode]),
+                                        dim3((unsigned)((sl.nodes + 255) / 256)), dim3(256), args, 0, ctx->stream));
+        }
         ctx->note_launch();
     }
 }

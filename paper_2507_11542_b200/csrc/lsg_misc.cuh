@@ -3,7 +3,7 @@
 
 #include <cuda_runtime.h>
 
-#include "lsg_kernels.cuh"
+#include "lsg_march3.cuh"
 
 namespace lsg {
 
@@ -21,6 +21,11 @@ struct ShapeParams {
 };
 
 using AlphaFn = void (*)(AlphaParams);
+
+March3Fn march3_lookup_linear(int s, int m);
+March3Fn march3_lookup_normal(int s, int m);
+March3Fn march3_lookup_rockets(int s, int m);
+March3Fn march3_lookup_air3d(int s, int m);
 
 StageFn stage_lookup_linear(int D, int s, int m);
 StageFn stage_lookup_normal(int D, int s, int m);

@@ -288,3 +288,37 @@ def test_cfg5_full_size_properties(ctx):
     slabs.set_field(v0)
     slabs.step(0.0, dt)
     assert_bitwise(slabs.get_field(), out0.ravel(), "4 slabs vs 1")
+
+
+@pytest.mark.parametrize("counts,periodic", [
+    ((300, 20, 9), ()),            # x-segment tiles with x-halo columns, extrapolated edges
+    ((300, 20, 9), (0, 1, 2)),     # wrapped x/y halo slots, periodic z window
+    ((257, 13, 11), (1,)),         # ragged last x tile (1 column), periodic y only
+    ((7, 300, 8), (0, 2)),         # tiny rows: many rows per tile, full-row periodic wrap
+    ((33, 7, 7), ()),              # minimum stencil room along y and z
+])
+def test_march3_tilings_vs_oracle(ctx, port, counts, periodic):
+    """The 2.5-D tiled 3-D kernel on awkward shapes, all schemes, bit for bit."""
+    g = abi.make_grid([-1.0, 0.0, 2.0], [1.0, 3.0, 5.0], list(counts), periodic)
+    v = H.random_field(g, sum(counts))
+    for s in range(4):
+        p = abi.make_problem(abi.HAM_LINEAR, s, abi.linear_params([0.7, -1.1, 0.4]), abi.GROW, s % 2 == 1)
+        a, ba = ctx.term_lf(g, p, 0.0, v)
+        b, bb = port.term_lf(g, p, 0.0, v)
+        assert ba == bb
+        assert_bitwise(a, b, f"term scheme {s}")
+        va, sa, _ = ctx.integrate(g, p, abi.CFL3, 0.0, 2.5 * 0.32 * ba, v)
+        vb, sb, _ = port.integrate(g, p, abi.CFL3, 0.0, 2.5 * 0.32 * bb, v)
+        assert_bitwise(sa, sb, f"steps scheme {s}")
+        assert_bitwise(va, vb, f"v scheme {s}")
+
+
+def test_generic_kernel_3d_still_exact(ctx, port, monkeypatch):
+    """LSG_KERNEL=generic forces the one-thread-per-node kernel on 3-D grids."""
+    monkeypatch.setenv("LSG_KERNEL", "generic")
+    S = P.cfg2_air3d(17)
+    v0 = H.initial_value(port, S)
+    va, sa, _ = ctx.integrate(S.grid, S.problem, S.method, 0.0, 0.03, v0)
+    vb, sb, _ = port.integrate(S.grid, S.problem, S.method, 0.0, 0.03, v0)
+    assert_bitwise(sa, sb, "steps")
+    assert_bitwise(va, vb, "v")
