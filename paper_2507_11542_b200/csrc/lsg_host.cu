@@ -209,12 +209,12 @@ StageFn lookup_stage(int kind, int D, int scheme, int mode) {
     return nullptr;
 }
 
-March3Fn lookup_march3(int kind, int scheme, int mode) {
+March3Fn lookup_march3(int kind, int scheme, int mode, bool range) {
     switch (kind) {
-        case LSG_HAM_LINEAR: return march3_lookup_linear(scheme, mode);
-        case LSG_HAM_NORMAL: return march3_lookup_normal(scheme, mode);
-        case LSG_HAM_ROCKETS: return march3_lookup_rockets(scheme, mode);
-        case LSG_HAM_AIR3D: return march3_lookup_air3d(scheme, mode);
+        case LSG_HAM_LINEAR: return march3_lookup_linear(scheme, mode, range);
+        case LSG_HAM_NORMAL: return march3_lookup_normal(scheme, mode, range);
+        case LSG_HAM_ROCKETS: return march3_lookup_rockets(scheme, mode, range);
+        case LSG_HAM_AIR3D: return march3_lookup_air3d(scheme, mode, range);
     }
     return nullptr;
 }
@@ -299,8 +299,10 @@ struct lsg_solver {
     unsigned alpha_flags = 0;
     double bound = 0.0;
     StageFn fn[3] = {nullptr, nullptr, nullptr};
-    March3Fn m3fn[3] = {nullptr, nullptr, nullptr};
+    March3Fn m3fn[3][2] = {};  // [mode][with v-range reduction]
     int m3_threads = 0;
+    int m3_pitch = 0;
+    int m3_per_sm = 1;
     size_t m3_smem = 0;
     std::string invalid;  // deferred invalid_argument (raised at the first term evaluation)
     int cur = 0;
@@ -355,32 +357,40 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             if (!s->fn[m]) s->invalid = "hamiltonian: kind not available for this grid dimension";
         }
 
-    // 2.5-D tiled kernel for 3-D grids (lsg_march3.cuh)
+    // 2.5-D tiled kernel for 3-D grids (lsg_march3.cuh): TX x R tiles, two
+    // x-adjacent nodes per thread, 256 threads per block.
     int TX = 0, R = 0;
     if (s->invalid.empty() && s->D == 3 && !force_generic()) {
         const int n0 = g->counts[0], n1 = g->counts[1];
         if (n0 <= 256) {
-            TX = n0;
-            R = std::max(2, 512 / n0);
+            TX = (n0 + 1) & ~1;  // full rows
+            R = std::max(1, 256 / (TX / 2));
         } else {
             TX = 32;
             R = 16;
         }
         R = std::min(R, n1);
         const int W = s->W;
-        const int threads = ((TX * R + 31) / 32) * 32;
-        const int halo = 2 * W * TX + (TX < n0 ? 2 * W * R : 0);
-        if (threads <= 512 && halo <= kMaxHalo * threads) {
+        const int threads = ((TX / 2 * R + 31) / 32) * 32;
+        const int halo = 2 * W * std::min(TX, n0) + 2 * W * R;
+        const long long padded_nodes = static_cast<long long>(g->counts[2] + 2 * W) * n0 * n1;
+        if (threads <= 256 && halo <= kMaxHalo * threads && padded_nodes < (1LL << 31) - 1) {
             bool all = true;
-            for (int m = 0; m < 3; ++m) {
-                s->m3fn[m] = lookup_march3(p->kind, p->scheme, m);
-                all = all && s->m3fn[m];
-            }
+            for (int m = 0; m < 3; ++m)
+                for (int r = 0; r < 2; ++r) {
+                    s->m3fn[m][r] = lookup_march3(p->kind, p->scheme, m, r == 1);
+                    all = all && s->m3fn[m][r];
+                }
             if (all) {
                 s->m3_threads = threads;
-                s->m3_smem = sizeof(double) * static_cast<size_t>((TX + 2 * W) * (R + 2 * W));
+                s->m3_pitch = (TX + 2 * W + (W & 1) + 2 + 1) & ~1;
+                s->m3_smem = sizeof(double) * static_cast<size_t>(s->m3_pitch * (R + 2 * W));
+                int per_sm = 0;
+                CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, reinterpret_cast<const void*>(s->m3fn[2][1]), threads, s->m3_smem));
+                s->m3_per_sm = std::max(1, per_sm);
             } else {
-                for (auto& f : s->m3fn) f = nullptr;
+                for (auto& fm : s->m3fn) fm[0] = fm[1] = nullptr;
             }
         }
     }
@@ -395,7 +405,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         if (s->P > 1 && sl.nz < s->W)
             fail(LSG_EINVAL, "slab decomposition: each slab needs at least " + std::to_string(s->W) + " planes");
         sl.nodes = static_cast<long long>(sl.nz) * s->plane;
-        if (s->m3fn[0]) {
+        if (s->m3fn[0][0]) {
             // tiles x z-chunks: minimise waves * (planes per chunk + warm-up) over 148 SMs
             const int ntx = (g->counts[0] + TX - 1) / TX, nty = (g->counts[1] + R - 1) / R;
             const int nt = ntx * nty;
@@ -404,7 +414,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             for (int nzc = 1; nzc <= sl.nz; ++nzc) {
                 const int chunk = (sl.nz + nzc - 1) / nzc;
                 const int used = (sl.nz + chunk - 1) / chunk;
-                const double waves = std::ceil(static_cast<double>(nt) * used / 148.0);
+                const double waves = std::ceil(static_cast<double>(nt) * used / (148.0 * s->m3_per_sm));
                 const double cost = waves * (chunk + 0.5 * s->W);
                 if (cost < best - 1e-9) {
                     best = cost;
@@ -412,7 +422,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                 }
             }
             const int chunk = (sl.nz + best_nzc - 1) / best_nzc;
-            sl.m3 = March3{TX, R, ntx, chunk};
+            sl.m3 = March3{TX, R, ntx, chunk, s->m3_pitch};
             sl.m3_grid = dim3(static_cast<unsigned>(nt), static_cast<unsigned>((sl.nz + chunk - 1) / chunk));
         }
         const long long padded = static_cast<long long>(sl.nz + 2 * s->halo_w) * s->plane;
@@ -588,9 +598,9 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
         std::memcpy(P.hp, s->p.params, sizeof P.hp);
         P.flags = s->dflags.as<unsigned>();
         P.range = range;
-        if (s->m3fn[mode]) {
+        if (s->m3fn[mode][0]) {
             void* args[] = {&P, &sl.m3};
-            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->m3fn[mode]), sl.m3_grid,
+            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), sl.m3_grid,
                                         dim3(static_cast<unsigned>(s->m3_threads)), args, s->m3_smem, ctx->stream));
         } else {
             void* args[] = {&P};

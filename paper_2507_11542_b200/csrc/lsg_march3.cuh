@@ -1,20 +1,20 @@
 // lsg_march3.cuh — 2.5-D tiled fused stage kernel for 3-D grids (sm_100a).
 //
-// Block = R full x-rows (R*n0 threads, one node each) of one y-tile, marching
-// along z through a chunk of planes.  Per plane:
-//   * the block stages the plane tile with W ghost rows above/below in shared
-//     memory (centre rows come from the threads' registers, halo rows are
-//     prefetched one plane ahead);
-//   * x- and y-windows are read from shared memory with the reference's
-//     ghost rules (grid.cpp:108-128) applied at the domain edges;
-//   * the z-window lives in registers and slides: one new value per plane,
-//     prefetched one plane ahead (ghost planes of a slab come from the halo
-//     buffer planes, global ghosts from the periodic wrap / extrapolation);
+// Block = a TX x R tile of the (x, y) plane, marching along z through a chunk
+// of planes.  Each thread owns two x-adjacent nodes (x, x+1), so the x-window
+// (2W+2 values) is shared by the pair, and every shared-memory access is a
+// 128-bit load of a node pair.  Per plane:
+//   * the tile and a W-wide halo ring (cross-shaped, no corners) are staged in
+//     shared memory: centre pairs come from the threads' registers, halo slots
+//     are prefetched one plane ahead and already hold the padded-line value
+//     (in-range node, periodic wrap, or the extrapolated ghost
+//     a + k*(a - b), grid.cpp:108-128), so every window is a plain read;
+//   * the z-windows of both nodes live in registers and slide one plane,
+//     the next value prefetched one plane ahead (slab halo planes / global
+//     ghosts resolved at load time, uniformly per block);
 //   * L/R per dimension, central costate, H, global-LF dissipation, clamp and
-//     the TVD-RK combination are fused exactly as in stage_kernel, so the
-//     result is bit-identical to it (and to the reference).
-// No index division per node, one global load per node per plane plus the
-// halo rows, one store.
+//     the TVD-RK combination use exactly the arithmetic of stage_kernel, so
+//     results are bit-identical to it and to the reference.
 #pragma once
 
 #include "lsg_kernels.cuh"
@@ -22,11 +22,14 @@
 namespace lsg {
 
 struct March3 {
-    int TX;      // tile width along x (== n0: full rows, no x-halo)
+    int TX;      // tile width along x (even)
     int R;       // tile height along y
     int ntx;     // tiles along x
     int zchunk;  // planes per block
+    int pitch;   // shared-memory row pitch in doubles (even)
 };
+
+constexpr int kMaxHalo = 4;  // halo slots per thread (the host picks tiles that respect it)
 
 template <int W>
 __device__ __forceinline__ double zvalue(const StageParams& P, long long base, int zz) {
@@ -49,69 +52,64 @@ __device__ __forceinline__ double zvalue(const StageParams& P, long long base, i
     return hi + (double)(zg - (ng - 1)) * (hi - x2);
 }
 
-// Window along a line of the staged tile: node j of the global line (n
-// nodes, tile origin o) sits at sm[off + (j - o + W) * st].  Out-of-range
-// nodes follow the ghost rule: periodic halo slots were loaded wrapped (or,
-// when the tile spans the whole line, the wrapped node is read directly);
-// extrapolation uses the edge nodes, which are inside the tile whenever a
-// ghost is needed (grid.cpp:108-128).
-template <int W>
-__device__ __forceinline__ void tile_window(const double* sm, int off, int st, int i, int o, int n, int bc,
-                                            bool full, double* s) {
-#pragma unroll
-    for (int k = -W; k <= W; ++k) {
-        const int j = i + k;
-        double v;
-        if (j >= 0 && j < n) {
-            v = sm[off + (j - o + W) * st];
-        } else if (bc == LSG_BC_PERIODIC) {
-            const int jj = full ? (j < 0 ? j + n : j - n) : j;
-            v = sm[off + (jj - o + W) * st];
-        } else if (j < 0) {
-            const double lo = sm[off + (0 - o + W) * st];
-            const double x1 = sm[off + (1 - o + W) * st];
-            v = lo + (double)(-j) * (lo - x1);
-        } else {
-            const double hi = sm[off + (n - 1 - o + W) * st];
-            const double x2 = sm[off + (n - 2 - o + W) * st];
-            v = hi + (double)(j - (n - 1)) * (hi - x2);
-        }
-        s[W + k] = v;
+// Finish one node: H, dissipation, clamp, RK combination; returns the output.
+template <int KIND, int MODE>
+__device__ __forceinline__ double finish_node(const StageParams& P, const double* xs, const int* ix,
+                                              const double* p, double diss, double centre, long long idx,
+                                              bool& bad) {
+    const double H = hamiltonian<KIND, 3>(P, xs, ix, p);
+    bad |= !isfinite(H);
+    double dv = -(H - 0.5 * diss);
+    if (P.restrict_update) dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
+    if constexpr (MODE == MODE_TERM) {
+        return dv;
+    } else if constexpr (MODE == MODE_EULER) {
+        return centre + P.dt * dv;
+    } else {
+        const double base = P.v0[idx];
+        return base + P.c * ((centre + P.dt * dv) - base);
     }
 }
 
-constexpr int kMaxHalo = 4;  // halo slots per thread (the host picks tiles that respect it)
-
-template <int S, int KIND, int MODE>
-__global__ void __launch_bounds__(512, 1) march3_kernel(const __grid_constant__ StageParams P,
+template <int S, int KIND, int MODE, bool RANGE>
+__global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ StageParams P,
                                                          const __grid_constant__ March3 M) {
     constexpr int W = SchemeWidth<S>::W;
-    extern __shared__ double sm[];
+    constexpr int SH = W & 1;                      // column shift that makes pair slots 16-byte aligned
+    constexpr int XW = (2 * W + 2 + SH + 1) & ~1;  // x-window doubles loaded (even)
+    extern __shared__ __align__(16) double sm[];
     const int n0 = P.n[0], n1 = P.n[1];
     const long long s2 = P.stride[2];
-    const int TX = M.TX, pitch = M.TX + 2 * W;
+    const int s2i = (int)s2;  // the host only picks this kernel for slabs below 2^31 nodes
+    const int TX = M.TX, pitch = M.pitch, TX2 = M.TX >> 1;
     const int t = threadIdx.x;
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
     const int cols = min(TX, n0 - x0), rows = min(M.R, n1 - y0);
-    const bool fullx = TX >= n0, fully = M.R >= n1;
     const int zs = blockIdx.y * M.zchunk;
     const int ze = min(zs + M.zchunk, P.n[2]);
-    const int yl = t / TX, xl = t - (t / TX) * TX;
+    const int yl = t / TX2, pl = t - (t / TX2) * TX2;
+    const int xl = 2 * pl;
     const bool active = yl < rows && xl < cols;
+    const bool two = active && xl + 1 < cols;
     const int x = x0 + (active ? xl : 0), y = y0 + (active ? yl : 0);
-    const long long col = (long long)y * n0 + x;  // offset of (x, y, 0)
-    const int me = (yl + W) * pitch + (xl + W);   // own slot
+    const long long col = (long long)y * n0 + x;      // offset of (x, y, 0)
+    const int coli = y * n0 + x;
+    const int me = (yl + W) * pitch + (xl + W + SH);  // own pair slot (even)
 
-    // halo slots of the cross-shaped tile: y-halo rows, then x-halo columns
+    // ---- halo slots ---------------------------------------------------------
     const int nyh = 2 * W * cols;
-    const int nxh = fullx ? 0 : 2 * W * rows;
-    int hsrc[kMaxHalo], hdst[kMaxHalo];
+    const int nxh = 2 * W * rows;
+    int hpa[kMaxHalo], hpb[kMaxHalo];  // 32-bit in-plane node offsets (-1: none)
+    int hdst[kMaxHalo];
+    double hk[kMaxHalo];
 #pragma unroll
     for (int q = 0; q < kMaxHalo; ++q) {
         const int h = t + q * blockDim.x;
-        hsrc[q] = -1;
+        hpa[q] = -1;
+        hpb[q] = -1;
         hdst[q] = -1;
+        hk[q] = 0.0;
         int r = 0, c = 0;
         bool use = false;
         if (h < nyh) {
@@ -127,95 +125,160 @@ __global__ void __launch_bounds__(512, 1) march3_kernel(const __grid_constant__ 
             use = true;
         }
         if (use) {
-            int gy = y0 - W + r, gx = x0 - W + c;
-            bool ok = true;
+            const int gy = y0 - W + r, gx = x0 - W + c;
+            int sy = gy, sx = gx, ey = -1, ex = -1;
             if (gy < 0 || gy >= n1) {
-                if (P.bc[1] == LSG_BC_PERIODIC && !fully) gy = gy < 0 ? gy + n1 : gy - n1;
-                else ok = false;
+                if (P.bc[1] == LSG_BC_PERIODIC) {
+                    sy = gy < 0 ? gy + n1 : gy - n1;
+                } else if (gy < 0) {
+                    sy = 0, ey = 1, hk[q] = (double)(-gy);
+                } else {
+                    sy = n1 - 1, ey = n1 - 2, hk[q] = (double)(gy - (n1 - 1));
+                }
             }
             if (gx < 0 || gx >= n0) {
-                if (P.bc[0] == LSG_BC_PERIODIC && !fullx) gx = gx < 0 ? gx + n0 : gx - n0;
-                else ok = false;
+                if (P.bc[0] == LSG_BC_PERIODIC) {
+                    sx = gx < 0 ? gx + n0 : gx - n0;
+                } else if (gx < 0) {
+                    sx = 0, ex = 1, hk[q] = (double)(-gx);
+                } else {
+                    sx = n0 - 1, ex = n0 - 2, hk[q] = (double)(gx - (n0 - 1));
+                }
             }
-            if (ok) {
-                hsrc[q] = gy * n0 + gx;
-                hdst[q] = r * pitch + c;
-            }
+            hpa[q] = sy * n0 + sx;
+            if (ey >= 0) hpb[q] = ey * n0 + sx;
+            if (ex >= 0) hpb[q] = sy * n0 + ex;
+            hdst[q] = r * pitch + c + SH;
         }
     }
 
-    // prologue: z-window for the first plane and its halo
-    double s[2 * W + 1];
+    // ---- prologue: z-windows of the pair and the first plane's halo ---------
+    double s0[2 * W + 1], s1[2 * W + 1];
 #pragma unroll
-    for (int j = 0; j < 2 * W + 1; ++j) s[j] = active ? zvalue<W>(P, col, zs - W + j) : 0.0;
-    double hv[kMaxHalo];
+    for (int j = 0; j < 2 * W + 1; ++j) {
+        s0[j] = active ? zvalue<W>(P, col, zs - W + j) : 0.0;
+        s1[j] = two ? zvalue<W>(P, col + 1, zs - W + j) : 0.0;
+    }
+    // raw prefetched halo values; the ghost formula is applied when staging so
+    // the loads of plane z+1 stay in flight while plane z is computed
+    double ha[kMaxHalo], hb[kMaxHalo];
 #pragma unroll
-    for (int q = 0; q < kMaxHalo; ++q) hv[q] = hsrc[q] >= 0 ? __ldg(P.u + hsrc[q] + (long long)zs * s2) : 0.0;
+    for (int q = 0; q < kMaxHalo; ++q) {
+        const int off = zs * s2i;
+        ha[q] = hpa[q] >= 0 ? __ldg(P.u + (hpa[q] + off)) : 0.0;
+        hb[q] = hpb[q] >= 0 ? __ldg(P.u + (hpb[q] + off)) : 0.0;
+    }
 
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
-    const double ax = __ldg(P.axis[0] + x), ay = __ldg(P.axis[1] + y);
+    const double ax0 = __ldg(P.axis[0] + x), ax1 = __ldg(P.axis[0] + x + (two ? 1 : 0));
+    const double ay = __ldg(P.axis[1] + y);
+    // planes z whose prefetch target z+1+W is a real in-slab plane need no ghost logic
+    const int zfast_lo = -P.z0 - 1 - W;
+    const int zfast_hi = P.nz_glob - P.z0 - 2 - W;
 
+#pragma unroll 2
     for (int z = zs; z < ze; ++z) {
         __syncthreads();
-        if (active) sm[me] = s[W];
+        if (two) *reinterpret_cast<double2*>(sm + me) = make_double2(s0[W], s1[W]);
+        else if (active) sm[me] = s0[W];  // me+1 is a ghost slot the halo pass fills
 #pragma unroll
         for (int q = 0; q < kMaxHalo; ++q)
-            if (hdst[q] >= 0) sm[hdst[q]] = hv[q];
-        // prefetch the next plane's window value and halo
-        double nxt = 0.0;
+            if (hdst[q] >= 0) sm[hdst[q]] = hpb[q] >= 0 ? ha[q] + hk[q] * (ha[q] - hb[q]) : ha[q];
+        // prefetch the next plane's window values and halo
+        double n0v = 0.0, n1v = 0.0;
         if (z + 1 < ze) {
-            if (active) nxt = zvalue<W>(P, col, z + 1 + W);
+            const int zn = z + 1 + W;
+            if (z >= zfast_lo && z <= zfast_hi) {  // uniform across the block
+                const int o = coli + zn * s2i;
+                if (active) {
+                    n0v = __ldg(P.u + o);
+                    n1v = __ldg(P.u + (o + (two ? 1 : 0)));
+                }
+            } else {
+                if (active) n0v = zvalue<W>(P, col, zn);
+                if (two) n1v = zvalue<W>(P, col + 1, zn);
+            }
+            const int off = (z + 1) * s2i;
 #pragma unroll
-            for (int q = 0; q < kMaxHalo; ++q)
-                if (hsrc[q] >= 0) hv[q] = __ldg(P.u + hsrc[q] + (long long)(z + 1) * s2);
+            for (int q = 0; q < kMaxHalo; ++q) {
+                if (hpa[q] >= 0) ha[q] = __ldg(P.u + (hpa[q] + off));
+                if (hpb[q] >= 0) hb[q] = __ldg(P.u + (hpb[q] + off));
+            }
         }
         __syncthreads();
         if (active) {
             const long long idx = col + (long long)z * s2;
             const int zg = P.z0 + z;
-            double xs[kMaxDim] = {ax, ay, __ldg(P.axis[2] + zg), 0, 0, 0};
-            int ix[kMaxDim] = {x, y, zg, 0, 0, 0};
-            double p[3];
-            double diss = 0.0;
-            double w[2 * W + 1];
+            const double az = __ldg(P.axis[2] + zg);
             double L, R;
-            tile_window<W>(sm, (yl + W) * pitch, 1, x, x0, n0, P.bc[0], fullx, w);
-            line_lr<S>(w, P.lc[0], L, R);
-            p[0] = 0.5 * (L + R);
-            diss += P.alpha[0] * (R - L);
-            tile_window<W>(sm, xl + W, pitch, y, y0, n1, P.bc[1], fully, w);
-            line_lr<S>(w, P.lc[1], L, R);
-            p[1] = 0.5 * (L + R);
-            diss += P.alpha[1] * (R - L);
-            line_lr<S>(s, P.lc[2], L, R);
-            p[2] = 0.5 * (L + R);
-            diss += P.alpha[2] * (R - L);
-            const double H = hamiltonian<KIND, 3>(P, xs, ix, p);
-            bad |= !isfinite(H);
-            double dv = -(H - 0.5 * diss);
-            if (P.restrict_update) dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
-            double o;
-            if constexpr (MODE == MODE_TERM) {
-                o = dv;
-            } else if constexpr (MODE == MODE_EULER) {
-                o = s[W] + P.dt * dv;
-            } else {
-                const double base = P.v0[idx];
-                o = base + P.c * ((s[W] + P.dt * dv) - base);
+            double pa[3], pb[3];
+            double da = 0.0, db = 0.0;
+            // x: 2W+2 consecutive padded-line values shared by the pair
+            double wx[XW];
+            const double* xrow = sm + me - W - SH;  // even (16-byte aligned) start
+#pragma unroll
+            for (int j = 0; j < XW; j += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(xrow + j);
+                wx[j] = v.x;
+                wx[j + 1] = v.y;
             }
-            P.out[idx] = o;
-            const unsigned long long key = order_key(o);
-            kmin = min(kmin, key);
-            kmax = max(kmax, key);
+            line_lr<S>(wx + SH, P.lc[0], L, R);
+            pa[0] = 0.5 * (L + R);
+            da += P.alpha[0] * (R - L);
+            line_lr<S>(wx + SH + 1, P.lc[0], L, R);
+            pb[0] = 0.5 * (L + R);
+            db += P.alpha[0] * (R - L);
+            // y: one 128-bit load per row gives both nodes' windows
+            double ya[2 * W + 1], yb[2 * W + 1];
+#pragma unroll
+            for (int k = -W; k <= W; ++k) {
+                const double2 v = *reinterpret_cast<const double2*>(sm + me + k * pitch);
+                ya[W + k] = v.x;
+                yb[W + k] = v.y;
+            }
+            line_lr<S>(ya, P.lc[1], L, R);
+            pa[1] = 0.5 * (L + R);
+            da += P.alpha[1] * (R - L);
+            line_lr<S>(yb, P.lc[1], L, R);
+            pb[1] = 0.5 * (L + R);
+            db += P.alpha[1] * (R - L);
+            // z: register windows
+            line_lr<S>(s0, P.lc[2], L, R);
+            pa[2] = 0.5 * (L + R);
+            da += P.alpha[2] * (R - L);
+            line_lr<S>(s1, P.lc[2], L, R);
+            pb[2] = 0.5 * (L + R);
+            db += P.alpha[2] * (R - L);
+            double xs[kMaxDim] = {ax0, ay, az, 0, 0, 0};
+            int ix[kMaxDim] = {x, y, zg, 0, 0, 0};
+            const double oa = finish_node<KIND, MODE>(P, xs, ix, pa, da, s0[W], idx, bad);
+            xs[0] = ax1;
+            ix[0] = x + (two ? 1 : 0);
+            bool bad_b = false;
+            const double ob = finish_node<KIND, MODE>(P, xs, ix, pb, db, s1[W], idx + (two ? 1 : 0), bad_b);
+            P.out[idx] = oa;
+            if (two) {
+                P.out[idx + 1] = ob;
+                bad |= bad_b;
+            }
+            if (RANGE) {
+                const unsigned long long ka = order_key(oa), kb = two ? order_key(ob) : ka;
+                kmin = min(kmin, min(ka, kb));
+                kmax = max(kmax, max(ka, kb));
+            }
         }
 #pragma unroll
-        for (int j = 0; j < 2 * W; ++j) s[j] = s[j + 1];
-        s[2 * W] = nxt;
+        for (int j = 0; j < 2 * W; ++j) {
+            s0[j] = s0[j + 1];
+            s1[j] = s1[j + 1];
+        }
+        s0[2 * W] = n0v;
+        s1[2 * W] = n1v;
     }
 
     if (P.flags && __any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
-    if (P.range) {
+    if (RANGE && P.range) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));

@@ -22,10 +22,10 @@ struct ShapeParams {
 
 using AlphaFn = void (*)(AlphaParams);
 
-March3Fn march3_lookup_linear(int s, int m);
-March3Fn march3_lookup_normal(int s, int m);
-March3Fn march3_lookup_rockets(int s, int m);
-March3Fn march3_lookup_air3d(int s, int m);
+March3Fn march3_lookup_linear(int s, int m, bool range);
+March3Fn march3_lookup_normal(int s, int m, bool range);
+March3Fn march3_lookup_rockets(int s, int m, bool range);
+March3Fn march3_lookup_air3d(int s, int m, bool range);
 
 StageFn stage_lookup_linear(int D, int s, int m);
 StageFn stage_lookup_normal(int D, int s, int m);
