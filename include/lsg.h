@@ -152,6 +152,10 @@ int lsg_grid_spacing(const lsg_grid* g, int d, double* dx);
 int lsg_grid_node_count(const lsg_grid* g, size_t* n);
 int lsg_grid_axis(const lsg_grid* g, int d, double* out);
 
+/* Slab of rank r among P along an axis of n planes: the first n % P ranks
+ * hold ceil(n/P) planes, the rest floor(n/P) (host-only, no device needed). */
+int lsg_slab_partition(int n, int nranks, int rank, int* z0, int* nz);
+
 /* ---- stateless reference-facing calls (host buffers in and out) ------------
  * Each call copies its host inputs to the device, runs the kernels, and copies
  * the results back; these are what a reference call site binds to. */

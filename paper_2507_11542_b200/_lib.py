@@ -22,7 +22,7 @@ EXPORTS = (
     "lsg_abi_version", "lsg_last_error", "lsg_opts_default", "lsg_device_count",
     "lsg_ctx_create", "lsg_nccl_unique_id", "lsg_ctx_create_dist", "lsg_ctx_destroy",
     "lsg_ctx_synchronize", "lsg_ctx_launch_count",
-    "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis",
+    "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis", "lsg_slab_partition",
     "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update",
     "lsg_integrate", "lsg_solve_brt",
     "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
@@ -268,6 +268,13 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     call("lsg_nccl_unique_id", buf)
     return bytes(buf)
+
+
+def slab_partition(n, nranks, rank):
+    """(z0, nz) of rank's slab along an axis of n planes (host-only)."""
+    z0, nz = C.c_int(), C.c_int()
+    call("lsg_slab_partition", C.c_int(n), C.c_int(nranks), C.c_int(rank), C.byref(z0), C.byref(nz))
+    return z0.value, nz.value
 
 
 def device_count():

@@ -889,6 +889,13 @@ int lsg_grid_axis(const lsg_grid* g, int d, double* out) {
     });
 }
 
+int lsg_slab_partition(int n, int nranks, int rank, int* z0, int* nz) {
+    return guarded([&] {
+        if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks) fail(LSG_EINVAL, "slab_partition: invalid arguments");
+        partition(n, nranks, rank, z0, nz);
+    });
+}
+
 int lsg_pad_ghost(lsg_ctx* ctx, const lsg_grid* g, const double* field, int dim, int width, double* out) {
     return guarded([&] {
         activate(ctx);
