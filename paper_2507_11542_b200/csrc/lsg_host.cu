@@ -384,7 +384,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             if (all) {
                 s->m3_threads = threads;
                 s->m3_pitch = (TX + 2 * W + (W & 1) + 2 + 1) & ~1;
-                s->m3_smem = sizeof(double) * static_cast<size_t>(s->m3_pitch * (R + 2 * W));
+                s->m3_smem = 2 * sizeof(double) * static_cast<size_t>(s->m3_pitch * (R + 2 * W));  // double-buffered tile
                 int per_sm = 0;
                 CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                     &per_sm, reinterpret_cast<const void*>(s->m3fn[2][1]), threads, s->m3_smem));

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ Stag
             p[d] = 0.5 * (L + R);              // hamiltonian.cpp:31-32
             diss += P.alpha[d] * (R - L);       // hamiltonian.cpp:60-64
         }
-        const double H = hamiltonian<KIND, D>(P, x, ix, p);
+        const double H = hamiltonian<KIND, D>(P, x, load_trig<KIND>(P, D > 2 ? ix[D > 2 ? 2 : 0] : 0, D > 5 ? ix[D > 5 ? 5 : 0] : 0), p);
         bad = !isfinite(H);                     // hamiltonian.cpp:38-40
         double dv = -(H - 0.5 * diss);          // hamiltonian.cpp:65
         if (P.restrict_update)                  // hamiltonian.cpp:78-88

@@ -54,10 +54,10 @@ __device__ __forceinline__ double zvalue(const StageParams& P, long long base, i
 
 // Finish one node: H, dissipation, clamp, RK combination; returns the output.
 template <int KIND, int MODE>
-__device__ __forceinline__ double finish_node(const StageParams& P, const double* xs, const int* ix,
-                                              const double* p, double diss, double centre, long long idx,
+__device__ __forceinline__ double finish_node(const StageParams& P, const double* xs, const Trig& tr,
+                                              const double* p, double diss, double centre, double base,
                                               bool& bad) {
-    const double H = hamiltonian<KIND, 3>(P, xs, ix, p);
+    const double H = hamiltonian<KIND, 3>(P, xs, tr, p);
     bad |= !isfinite(H);
     double dv = -(H - 0.5 * diss);
     if (P.restrict_update) dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
@@ -66,7 +66,6 @@ __device__ __forceinline__ double finish_node(const StageParams& P, const double
     } else if constexpr (MODE == MODE_EULER) {
         return centre + P.dt * dv;
     } else {
-        const double base = P.v0[idx];
         return base + P.c * ((centre + P.dt * dv) - base);
     }
 }
@@ -152,22 +151,37 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
         }
     }
 
-    // ---- prologue: z-windows of the pair and the first plane's halo ---------
+    // ---- prologue ------------------------------------------------------------
     double s0[2 * W + 1], s1[2 * W + 1];
 #pragma unroll
     for (int j = 0; j < 2 * W + 1; ++j) {
         s0[j] = active ? zvalue<W>(P, col, zs - W + j) : 0.0;
         s1[j] = two ? zvalue<W>(P, col + 1, zs - W + j) : 0.0;
     }
-    // raw prefetched halo values; the ghost formula is applied when staging so
-    // the loads of plane z+1 stay in flight while plane z is computed
+    // Raw halo values (the ghost formula is applied when staging, so loads stay
+    // in flight): ha/hb hold the plane staged next.
     double ha[kMaxHalo], hb[kMaxHalo];
+    auto load_halo = [&](int zz) {
+        const int off = zz * s2i;
 #pragma unroll
-    for (int q = 0; q < kMaxHalo; ++q) {
-        const int off = zs * s2i;
-        ha[q] = hpa[q] >= 0 ? __ldg(P.u + (hpa[q] + off)) : 0.0;
-        hb[q] = hpb[q] >= 0 ? __ldg(P.u + (hpb[q] + off)) : 0.0;
-    }
+        for (int q = 0; q < kMaxHalo; ++q) {
+            if (hpa[q] >= 0) ha[q] = __ldg(P.u + (hpa[q] + off));
+            if (hpb[q] >= 0) hb[q] = __ldg(P.u + (hpb[q] + off));
+        }
+    };
+    auto stage_plane = [&](double* buf, double c0, double c1) {
+        if (two) *reinterpret_cast<double2*>(buf + me) = make_double2(c0, c1);
+        else if (active) buf[me] = c0;  // me+1 is a ghost slot the halo pass fills
+#pragma unroll
+        for (int q = 0; q < kMaxHalo; ++q)
+            if (hdst[q] >= 0) buf[hdst[q]] = hpb[q] >= 0 ? ha[q] + hk[q] * (ha[q] - hb[q]) : ha[q];
+    };
+#pragma unroll
+    for (int q = 0; q < kMaxHalo; ++q) ha[q] = hb[q] = 0.0;
+    load_halo(zs);
+    double* const bufs[2] = {sm, sm + pitch * (M.R + 2 * W)};
+    stage_plane(bufs[0], s0[W], s1[W]);
+    if (zs + 1 < ze) load_halo(zs + 1);
 
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
@@ -176,17 +190,27 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     // planes z whose prefetch target z+1+W is a real in-slab plane need no ghost logic
     const int zfast_lo = -P.z0 - 1 - W;
     const int zfast_hi = P.nz_glob - P.z0 - 2 - W;
+    // per-plane operands, prefetched one plane ahead
+    double az = __ldg(P.axis[2] + P.z0 + zs);
+    Trig tr = load_trig<KIND>(P, P.z0 + zs, 0);
+    double b0 = 0.0, b1 = 0.0;
+    if (MODE == MODE_COMBINE && active) {
+        const int o = coli + zs * s2i;
+        b0 = P.v0[o];
+        b1 = P.v0[o + (two ? 1 : 0)];
+    }
+    __syncthreads();
 
-#pragma unroll 2
     for (int z = zs; z < ze; ++z) {
-        __syncthreads();
-        if (two) *reinterpret_cast<double2*>(sm + me) = make_double2(s0[W], s1[W]);
-        else if (active) sm[me] = s0[W];  // me+1 is a ghost slot the halo pass fills
-#pragma unroll
-        for (int q = 0; q < kMaxHalo; ++q)
-            if (hdst[q] >= 0) sm[hdst[q]] = hpb[q] >= 0 ? ha[q] + hk[q] * (ha[q] - hb[q]) : ha[q];
-        // prefetch the next plane's window values and halo
-        double n0v = 0.0, n1v = 0.0;
+        double* const cur = bufs[(z - zs) & 1];
+        // stage plane z+1 into the other buffer (its centre is already in the window)
+        if (z + 1 < ze) {
+            stage_plane(bufs[(z - zs + 1) & 1], s0[W + 1], s1[W + 1]);
+            if (z + 2 < ze) load_halo(z + 2);
+        }
+        // prefetch the next window value and the next plane's operands
+        double n0v = 0.0, n1v = 0.0, azn = 0.0, nb0 = 0.0, nb1 = 0.0;
+        Trig trn;
         if (z + 1 < ze) {
             const int zn = z + 1 + W;
             if (z >= zfast_lo && z <= zfast_hi) {  // uniform across the block
@@ -199,24 +223,23 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
                 if (active) n0v = zvalue<W>(P, col, zn);
                 if (two) n1v = zvalue<W>(P, col + 1, zn);
             }
-            const int off = (z + 1) * s2i;
-#pragma unroll
-            for (int q = 0; q < kMaxHalo; ++q) {
-                if (hpa[q] >= 0) ha[q] = __ldg(P.u + (hpa[q] + off));
-                if (hpb[q] >= 0) hb[q] = __ldg(P.u + (hpb[q] + off));
+            azn = __ldg(P.axis[2] + P.z0 + z + 1);
+            trn = load_trig<KIND>(P, P.z0 + z + 1, 0);
+            if (MODE == MODE_COMBINE && active) {
+                const int o = coli + (z + 1) * s2i;
+                nb0 = P.v0[o];
+                nb1 = P.v0[o + (two ? 1 : 0)];
             }
         }
-        __syncthreads();
         if (active) {
-            const long long idx = col + (long long)z * s2;
-            const int zg = P.z0 + z;
-            const double az = __ldg(P.axis[2] + zg);
+            const int idx = coli + z * s2i;
+            const int me_ = me;
             double L, R;
             double pa[3], pb[3];
             double da = 0.0, db = 0.0;
             // x: 2W+2 consecutive padded-line values shared by the pair
             double wx[XW];
-            const double* xrow = sm + me - W - SH;  // even (16-byte aligned) start
+            const double* xrow = cur + me_ - W - SH;  // even (16-byte aligned) start
 #pragma unroll
             for (int j = 0; j < XW; j += 2) {
                 const double2 v = *reinterpret_cast<const double2*>(xrow + j);
@@ -233,7 +256,7 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
             double ya[2 * W + 1], yb[2 * W + 1];
 #pragma unroll
             for (int k = -W; k <= W; ++k) {
-                const double2 v = *reinterpret_cast<const double2*>(sm + me + k * pitch);
+                const double2 v = *reinterpret_cast<const double2*>(cur + me_ + k * pitch);
                 ya[W + k] = v.x;
                 yb[W + k] = v.y;
             }
@@ -250,13 +273,11 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
             line_lr<S>(s1, P.lc[2], L, R);
             pb[2] = 0.5 * (L + R);
             db += P.alpha[2] * (R - L);
-            double xs[kMaxDim] = {ax0, ay, az, 0, 0, 0};
-            int ix[kMaxDim] = {x, y, zg, 0, 0, 0};
-            const double oa = finish_node<KIND, MODE>(P, xs, ix, pa, da, s0[W], idx, bad);
+            double xs[3] = {ax0, ay, az};
+            const double oa = finish_node<KIND, MODE>(P, xs, tr, pa, da, s0[W], b0, bad);
             xs[0] = ax1;
-            ix[0] = x + (two ? 1 : 0);
             bool bad_b = false;
-            const double ob = finish_node<KIND, MODE>(P, xs, ix, pb, db, s1[W], idx + (two ? 1 : 0), bad_b);
+            const double ob = finish_node<KIND, MODE>(P, xs, tr, pb, db, s1[W], b1, bad_b);
             P.out[idx] = oa;
             if (two) {
                 P.out[idx + 1] = ob;
@@ -275,6 +296,11 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
         }
         s0[2 * W] = n0v;
         s1[2 * W] = n1v;
+        az = azn;
+        tr = trn;
+        b0 = nb0;
+        b1 = nb1;
+        __syncthreads();  // plane z+1 staged; everyone is done reading plane z's buffer
     }
 
     if (P.flags && __any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);

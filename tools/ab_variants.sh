@@ -9,5 +9,5 @@ run() {
   python bench.py --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/v.json 2>/dev/null
   python -c "import json; d=json.load(open('gpurun_out/v.json')); print('minB=$1 unroll=$2:', round(d['value']/1e9,2), 'G pt-stage/s', [round(x*1e3,1) for x in d['config']['stage_ms_mean']], 'frac', round(d['roofline']['frac'],3))"
 }
-run 2 1; run 2 2; run 1 1; run 1 2
+run 2 1; run 1 1
 cp /tmp/orig.cuh $F
