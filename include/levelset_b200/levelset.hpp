@@ -145,6 +145,7 @@ struct HamiltonianProblem {
     UpdateDirection update_direction = UpdateDirection::Grow;
     bool restrict_update = false;
     DeviceHamiltonian device;            // what the B200 path evaluates
+    unsigned options = 0;                // LSG_OPT_* (e.g. LSG_OPT_WENO5_FAST)
 };
 
 struct TermResult {

@@ -106,8 +106,15 @@ typedef struct lsg_problem {
     int scheme;          /* costate_scheme, LSG_SCHEME_* */
     int direction;       /* update_direction, LSG_GROW / LSG_SHRINK */
     int restrict_update; /* bool */
+    int options;         /* LSG_OPT_* bits */
     double params[LSG_MAX_PARAMS];
 } lsg_problem;
+
+/* lsg_problem.options: WENO5 with one division per side (common-denominator
+ * weights, constant reciprocals) instead of the reference's 13; results agree
+ * with the reference within a few ulps per derivative (north_star: 1e-10
+ * relative), not bit for bit.  Off by default. */
+#define LSG_OPT_WENO5_FAST 1u
 
 /* IntegratorOptions (integrator.hpp:14-24). */
 typedef struct lsg_opts {

@@ -46,6 +46,7 @@ class LsgProblem(C.Structure):
         ("scheme", C.c_int),
         ("direction", C.c_int),
         ("restrict_update", C.c_int),
+        ("options", C.c_int),
         ("params", C.c_double * MAX_PARAMS),
     ]
 
@@ -88,8 +89,12 @@ def make_grid(mins, maxs, counts, periodic_dims=()) -> LsgGrid:
     return g
 
 
-def make_problem(kind, scheme, params=(), direction=GROW, restrict_update=False) -> LsgProblem:
+OPT_WENO5_FAST = 1
+
+
+def make_problem(kind, scheme, params=(), direction=GROW, restrict_update=False, options=0) -> LsgProblem:
     p = LsgProblem()
+    p.options = int(options)
     p.kind = int(kind)
     p.scheme = int(scheme)
     p.direction = int(direction)

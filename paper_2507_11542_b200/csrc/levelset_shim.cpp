@@ -74,6 +74,7 @@ lsg_problem to_c(const HamiltonianProblem& p) {
     c.scheme = scheme_c(p.costate_scheme);
     c.direction = p.update_direction == UpdateDirection::Shrink ? LSG_SHRINK : LSG_GROW;
     c.restrict_update = p.restrict_update ? 1 : 0;
+    c.options = static_cast<int>(p.options);
     for (int k = 0; k < LSG_MAX_PARAMS; ++k) c.params[k] = p.device.params[static_cast<std::size_t>(k)];
     return c;
 }

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -351,9 +352,11 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         if (g->counts[d] < min_nodes(p->scheme))
             s->invalid = std::string(scheme_name(p->scheme)) + ": needs at least " +
                          std::to_string(min_nodes(p->scheme)) + " nodes along dim " + std::to_string(d);
+    // kernel scheme id: the opt-in one-division WENO5 is a separate instantiation
+    const int kscheme = (p->scheme == LSG_SCHEME_WENO5 && (p->options & LSG_OPT_WENO5_FAST)) ? WENO5F : p->scheme;
     if (s->invalid.empty())
         for (int m = 0; m < 3; ++m) {
-            s->fn[m] = lookup_stage(p->kind, s->D, p->scheme, m);
+            s->fn[m] = lookup_stage(p->kind, s->D, kscheme, m);
             if (!s->fn[m]) s->invalid = "hamiltonian: kind not available for this grid dimension";
         }
 
@@ -369,6 +372,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             TX = 32;
             R = 16;
         }
+        if (const char* e = std::getenv("LSG_M3_R")) R = std::max(1, std::atoi(e));
         R = std::min(R, n1);
         const int W = s->W;
         const int threads = ((TX / 2 * R + 31) / 32) * 32;
@@ -378,13 +382,21 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             bool all = true;
             for (int m = 0; m < 3; ++m)
                 for (int r = 0; r < 2; ++r) {
-                    s->m3fn[m][r] = lookup_march3(p->kind, p->scheme, m, r == 1);
+                    s->m3fn[m][r] = lookup_march3(p->kind, kscheme, m, r == 1);
                     all = all && s->m3fn[m][r];
                 }
             if (all) {
                 s->m3_threads = threads;
-                s->m3_pitch = (TX + 2 * W + (W & 1) + 2 + 1) & ~1;
-                s->m3_smem = 2 * sizeof(double) * static_cast<size_t>(s->m3_pitch * (R + 2 * W));  // double-buffered tile
+                const int Wr = s->W, SHr = Wr & 1, XWr = (2 * Wr + 2 + SHr + 1) & ~1;
+                s->m3_pitch = (TX + XWr - 2 + 1) & ~1;
+                const int NB = 2 * Wr + 1 + 2, NV = 3;  // RingShape<W>
+                s->m3_smem = sizeof(double) * static_cast<size_t>(NB * s->m3_pitch * (R + 2 * Wr) + NV * TX * R);
+                if (s->m3_smem > 48 * 1024)
+                    for (int m = 0; m < 3; ++m)
+                        for (int r = 0; r < 2; ++r)
+                            CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->m3fn[m][r]),
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            static_cast<int>(s->m3_smem)));
                 int per_sm = 0;
                 CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                     &per_sm, reinterpret_cast<const void*>(s->m3fn[2][1]), threads, s->m3_smem));
@@ -415,13 +427,17 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                 const int chunk = (sl.nz + nzc - 1) / nzc;
                 const int used = (sl.nz + chunk - 1) / chunk;
                 const double waves = std::ceil(static_cast<double>(nt) * used / (148.0 * s->m3_per_sm));
-                const double cost = waves * (chunk + 0.5 * s->W);
+                const double cost = waves * (chunk + 0.5 * s->W + 1.0);
                 if (cost < best - 1e-9) {
                     best = cost;
                     best_nzc = used;
                 }
             }
-            const int chunk = (sl.nz + best_nzc - 1) / best_nzc;
+            int chunk = (sl.nz + best_nzc - 1) / best_nzc;
+            if (const char* e = std::getenv("LSG_M3_CHUNK")) chunk = std::max(1, std::min(sl.nz, std::atoi(e)));
+            if (std::getenv("LSG_M3_VERBOSE"))
+                std::fprintf(stderr, "march3: TX=%d R=%d tiles=%d chunk=%d blocks/SM=%d smem=%zu threads=%d\n", TX, R,
+                             nt, chunk, s->m3_per_sm, s->m3_smem, s->m3_threads);
             sl.m3 = March3{TX, R, ntx, chunk, s->m3_pitch};
             sl.m3_grid = dim3(static_cast<unsigned>(nt), static_cast<unsigned>((sl.nz + chunk - 1) / chunk));
         }

@@ -29,7 +29,7 @@ struct March3 {
     int pitch;   // shared-memory row pitch in doubles (even)
 };
 
-constexpr int kMaxHalo = 4;  // halo slots per thread (the host picks tiles that respect it)
+constexpr int kMaxHalo = 3;  // halo slots per thread (the host picks tiles that respect it)
 
 template <int W>
 __device__ __forceinline__ double zvalue(const StageParams& P, long long base, int zz) {
@@ -70,17 +70,40 @@ __device__ __forceinline__ double finish_node(const StageParams& P, const double
     }
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Ring geometry shared by host and device.
+template <int W>
+struct RingShape {
+    static constexpr int D = 2;              // planes in flight ahead of the newest plane needed
+    static constexpr int NB = 2 * W + 1 + D; // u planes resident: z-W .. z+W+D
+    static constexpr int NV = D + 1;         // v0 planes resident: z .. z+D
+    static constexpr int SH = W & 1;         // column shift: node-pair slots 16-byte aligned
+    static constexpr int XW = (2 * W + 2 + SH + 1) & ~1;  // x-window doubles loaded per pair
+};
+
 template <int S, int KIND, int MODE, bool RANGE>
 __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ StageParams P,
                                                          const __grid_constant__ March3 M) {
     constexpr int W = SchemeWidth<S>::W;
-    constexpr int SH = W & 1;                      // column shift that makes pair slots 16-byte aligned
-    constexpr int XW = (2 * W + 2 + SH + 1) & ~1;  // x-window doubles loaded (even)
+    using RS = RingShape<W>;
+    constexpr int D = RS::D, NB = RS::NB, NV = RS::NV, SH = RS::SH, XW = RS::XW;
     extern __shared__ __align__(16) double sm[];
     const int n0 = P.n[0], n1 = P.n[1];
     const long long s2 = P.stride[2];
-    const int s2i = (int)s2;  // the host only picks this kernel for slabs below 2^31 nodes
     const int TX = M.TX, pitch = M.pitch, TX2 = M.TX >> 1;
+    const int plane_sz = pitch * (M.R + 2 * W);
+    const int vplane_sz = TX * M.R;
+    double* const ring = sm;
+    double* const vring = sm + NB * plane_sz;
     const int t = threadIdx.x;
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
@@ -92,23 +115,19 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     const bool active = yl < rows && xl < cols;
     const bool two = active && xl + 1 < cols;
     const int x = x0 + (active ? xl : 0), y = y0 + (active ? yl : 0);
-    const long long col = (long long)y * n0 + x;      // offset of (x, y, 0)
-    const int coli = y * n0 + x;
+    const int coli = y * n0 + x;                      // in-plane offset of (x, y)
     const int me = (yl + W) * pitch + (xl + W + SH);  // own pair slot (even)
+    const int vme = yl * TX + xl;                     // own pair slot in the v0 ring (even)
 
-    // ---- halo slots ---------------------------------------------------------
+    // ---- halo slots: copies from global, or ghosts computed in shared memory
     const int nyh = 2 * W * cols;
     const int nxh = 2 * W * rows;
-    int hpa[kMaxHalo], hpb[kMaxHalo];  // 32-bit in-plane node offsets (-1: none)
-    int hdst[kMaxHalo];
-    double hk[kMaxHalo];
+    int hsrc[kMaxHalo], hdst[kMaxHalo], ga[kMaxHalo], gb[kMaxHalo];
+    double gk[kMaxHalo];
 #pragma unroll
     for (int q = 0; q < kMaxHalo; ++q) {
         const int h = t + q * blockDim.x;
-        hpa[q] = -1;
-        hpb[q] = -1;
-        hdst[q] = -1;
-        hk[q] = 0.0;
+        hsrc[q] = -1, hdst[q] = -1, ga[q] = 0, gb[q] = 0, gk[q] = 0.0;
         int r = 0, c = 0;
         bool use = false;
         if (h < nyh) {
@@ -124,160 +143,199 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
             use = true;
         }
         if (use) {
-            const int gy = y0 - W + r, gx = x0 - W + c;
-            int sy = gy, sx = gx, ey = -1, ex = -1;
+            int gy = y0 - W + r, gx = x0 - W + c;
+            hdst[q] = r * pitch + c + SH;
+            bool ghost = false;
             if (gy < 0 || gy >= n1) {
                 if (P.bc[1] == LSG_BC_PERIODIC) {
-                    sy = gy < 0 ? gy + n1 : gy - n1;
-                } else if (gy < 0) {
-                    sy = 0, ey = 1, hk[q] = (double)(-gy);
-                } else {
-                    sy = n1 - 1, ey = n1 - 2, hk[q] = (double)(gy - (n1 - 1));
+                    gy = gy < 0 ? gy + n1 : gy - n1;
+                } else {  // dst[w-k] = lo + k*(lo - x1): edge rows are inside the tile
+                    const int e0 = gy < 0 ? 0 : n1 - 1, e1 = gy < 0 ? 1 : n1 - 2;
+                    ga[q] = (e0 - y0 + W) * pitch + c + SH;
+                    gb[q] = (e1 - y0 + W) * pitch + c + SH;
+                    gk[q] = (double)(gy < 0 ? -gy : gy - (n1 - 1));
+                    ghost = true;
                 }
             }
             if (gx < 0 || gx >= n0) {
                 if (P.bc[0] == LSG_BC_PERIODIC) {
-                    sx = gx < 0 ? gx + n0 : gx - n0;
-                } else if (gx < 0) {
-                    sx = 0, ex = 1, hk[q] = (double)(-gx);
+                    gx = gx < 0 ? gx + n0 : gx - n0;
                 } else {
-                    sx = n0 - 1, ex = n0 - 2, hk[q] = (double)(gx - (n0 - 1));
+                    const int e0 = gx < 0 ? 0 : n0 - 1, e1 = gx < 0 ? 1 : n0 - 2;
+                    ga[q] = r * pitch + (e0 - x0 + W) + SH;
+                    gb[q] = r * pitch + (e1 - x0 + W) + SH;
+                    gk[q] = (double)(gx < 0 ? -gx : gx - (n0 - 1));
+                    ghost = true;
                 }
             }
-            hpa[q] = sy * n0 + sx;
-            if (ey >= 0) hpb[q] = ey * n0 + sx;
-            if (ex >= 0) hpb[q] = sy * n0 + ex;
-            hdst[q] = r * pitch + c + SH;
+            if (!ghost) hsrc[q] = gy * n0 + gx;
         }
     }
 
-    // ---- prologue ------------------------------------------------------------
-    double s0[2 * W + 1], s1[2 * W + 1];
+    const int nglob = P.nz_glob;
+    auto uslot = [&](int p) { return ring + ((p - zs + W) % NB) * plane_sz; };
+    auto vslot = [&](int p) { return vring + ((p - zs) % NV) * vplane_sz; };
+
+    // Issue the async copies of u-plane p (chunk-relative window [zs-W, ze+W))
+    // and of v0-plane p-W, as one commit group.
+    auto issue = [&](int p) {
+        if (p < ze + W) {
+            double* buf = uslot(p);
+            const int zg = P.z0 + p;
+            int src = p;
+            bool ghost_plane = false;
+            if (zg < 0 || zg >= nglob) {
+                if (P.bc[2] == LSG_BC_PERIODIC) src = P.halo ? p : (zg < 0 ? p + nglob : p - nglob);
+                else ghost_plane = true;
+            }
+            if (!ghost_plane) {
+                const double* base = P.u + (long long)src * s2;
+                if (active) cp_async8(buf + me, base + coli);
+                if (two) cp_async8(buf + me + 1, base + coli + 1);
 #pragma unroll
-    for (int j = 0; j < 2 * W + 1; ++j) {
-        s0[j] = active ? zvalue<W>(P, col, zs - W + j) : 0.0;
-        s1[j] = two ? zvalue<W>(P, col + 1, zs - W + j) : 0.0;
-    }
-    // Raw halo values (the ghost formula is applied when staging, so loads stay
-    // in flight): ha/hb hold the plane staged next.
-    double ha[kMaxHalo], hb[kMaxHalo];
-    auto load_halo = [&](int zz) {
-        const int off = zz * s2i;
+                for (int q = 0; q < kMaxHalo; ++q)
+                    if (hsrc[q] >= 0) cp_async8(buf + hdst[q], base + hsrc[q]);
+            } else {
+                // extrapolated plane beyond a global boundary (grid.cpp:120-126): plain loads
+                const int e0 = zg < 0 ? 0 : nglob - 1, e1 = zg < 0 ? 1 : nglob - 2;
+                const double k = (double)(zg < 0 ? -zg : zg - (nglob - 1));
+                const double* b0 = P.u + (long long)(e0 - P.z0) * s2;
+                const double* b1 = P.u + (long long)(e1 - P.z0) * s2;
+                auto ext = [&](int o) {
+                    const double lo = __ldg(b0 + o);
+                    return lo + k * (lo - __ldg(b1 + o));
+                };
+                if (active) buf[me] = ext(coli);
+                if (two) buf[me + 1] = ext(coli + 1);
 #pragma unroll
-        for (int q = 0; q < kMaxHalo; ++q) {
-            if (hpa[q] >= 0) ha[q] = __ldg(P.u + (hpa[q] + off));
-            if (hpb[q] >= 0) hb[q] = __ldg(P.u + (hpb[q] + off));
+                for (int q = 0; q < kMaxHalo; ++q)
+                    if (hsrc[q] >= 0) buf[hdst[q]] = ext(hsrc[q]);
+            }
         }
+        if (MODE == MODE_COMBINE) {
+            const int pv = p - W;
+            if (pv >= zs && pv < ze) {
+                double* vb = vslot(pv);
+                const double* base = P.v0 + (long long)pv * s2;
+                if (active) cp_async8(vb + vme, base + coli);
+                if (two) cp_async8(vb + vme + 1, base + coli + 1);
+            }
+        }
+        cp_async_commit();
     };
-    auto stage_plane = [&](double* buf, double c0, double c1) {
-        if (two) *reinterpret_cast<double2*>(buf + me) = make_double2(c0, c1);
-        else if (active) buf[me] = c0;  // me+1 is a ghost slot the halo pass fills
+    auto ghost_pass = [&](int p) {
+        if (p >= ze + W) return;
+        double* buf = uslot(p);
 #pragma unroll
         for (int q = 0; q < kMaxHalo; ++q)
-            if (hdst[q] >= 0) buf[hdst[q]] = hpb[q] >= 0 ? ha[q] + hk[q] * (ha[q] - hb[q]) : ha[q];
+            if (hdst[q] >= 0 && hsrc[q] < 0) {
+                const double a = buf[ga[q]];
+                buf[hdst[q]] = a + gk[q] * (a - buf[gb[q]]);
+            }
     };
-#pragma unroll
-    for (int q = 0; q < kMaxHalo; ++q) ha[q] = hb[q] = 0.0;
-    load_halo(zs);
-    double* const bufs[2] = {sm, sm + pitch * (M.R + 2 * W)};
-    stage_plane(bufs[0], s0[W], s1[W]);
-    if (zs + 1 < ze) load_halo(zs + 1);
+
+    // ---- prologue: u-planes zs-W .. zs+W+D-1 in flight, then the first 2W+1 resident
+#pragma unroll 1
+    for (int p = zs - W; p < zs + W + D; ++p) issue(p);
+    cp_async_wait<D>();  // groups up to u-plane zs+W-1 complete
+    __syncthreads();
+#pragma unroll 1
+    for (int p = zs - W; p < zs + W; ++p) ghost_pass(p);
 
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
     const double ax0 = __ldg(P.axis[0] + x), ax1 = __ldg(P.axis[0] + x + (two ? 1 : 0));
     const double ay = __ldg(P.axis[1] + y);
-    // planes z whose prefetch target z+1+W is a real in-slab plane need no ghost logic
-    const int zfast_lo = -P.z0 - 1 - W;
-    const int zfast_hi = P.nz_glob - P.z0 - 2 - W;
-    // per-plane operands, prefetched one plane ahead
     double az = __ldg(P.axis[2] + P.z0 + zs);
     Trig tr = load_trig<KIND>(P, P.z0 + zs, 0);
-    double b0 = 0.0, b1 = 0.0;
-    if (MODE == MODE_COMBINE && active) {
-        const int o = coli + zs * s2i;
-        b0 = P.v0[o];
-        b1 = P.v0[o + (two ? 1 : 0)];
-    }
-    __syncthreads();
 
+    int j0 = 0;  // ring slot of plane z-W (advances by one per plane)
+#pragma unroll 1
     for (int z = zs; z < ze; ++z) {
-        double* const cur = bufs[(z - zs) & 1];
-        // stage plane z+1 into the other buffer (its centre is already in the window)
-        if (z + 1 < ze) {
-            stage_plane(bufs[(z - zs + 1) & 1], s0[W + 1], s1[W + 1]);
-            if (z + 2 < ze) load_halo(z + 2);
+        cp_async_wait<D - 1>();  // u-plane z+W (and v0-plane z) complete for this thread
+        __syncthreads();         // ... and for every thread; slot of z-W-1 is free
+        ghost_pass(z + W);
+        issue(z + W + D);
+        // the 2W+1 resident planes z-W..z+W sit in ring slots j0, j0+1, ... (mod NB)
+        const double* zpl[2 * W + 1];
+#pragma unroll
+        for (int k = 0; k < 2 * W + 1; ++k) {
+            const int j = j0 + k;
+            zpl[k] = ring + (j >= NB ? j - NB : j) * plane_sz + me;
         }
-        // prefetch the next window value and the next plane's operands
-        double n0v = 0.0, n1v = 0.0, azn = 0.0, nb0 = 0.0, nb1 = 0.0;
+        j0 = j0 + 1 == NB ? 0 : j0 + 1;
+        double azn = 0.0;
         Trig trn;
         if (z + 1 < ze) {
-            const int zn = z + 1 + W;
-            if (z >= zfast_lo && z <= zfast_hi) {  // uniform across the block
-                const int o = coli + zn * s2i;
-                if (active) {
-                    n0v = __ldg(P.u + o);
-                    n1v = __ldg(P.u + (o + (two ? 1 : 0)));
-                }
-            } else {
-                if (active) n0v = zvalue<W>(P, col, zn);
-                if (two) n1v = zvalue<W>(P, col + 1, zn);
-            }
             azn = __ldg(P.axis[2] + P.z0 + z + 1);
             trn = load_trig<KIND>(P, P.z0 + z + 1, 0);
-            if (MODE == MODE_COMBINE && active) {
-                const int o = coli + (z + 1) * s2i;
-                nb0 = P.v0[o];
-                nb1 = P.v0[o + (two ? 1 : 0)];
-            }
         }
         if (active) {
-            const int idx = coli + z * s2i;
-            const int me_ = me;
+            const double* cur = zpl[W] - me;
+            const int idx = coli + z * (int)s2;
             double L, R;
             double pa[3], pb[3];
             double da = 0.0, db = 0.0;
-            // x: 2W+2 consecutive padded-line values shared by the pair
-            double wx[XW];
-            const double* xrow = cur + me_ - W - SH;  // even (16-byte aligned) start
+            {   // x: 2W+2 consecutive padded-line values shared by the pair
+                double wx[XW];
+                const double* xrow = cur + me - W - SH;
 #pragma unroll
-            for (int j = 0; j < XW; j += 2) {
-                const double2 v = *reinterpret_cast<const double2*>(xrow + j);
-                wx[j] = v.x;
-                wx[j + 1] = v.y;
+                for (int j = 0; j < XW; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(xrow + j);
+                    wx[j] = v.x;
+                    wx[j + 1] = v.y;
+                }
+                line_lr<S>(wx + SH, P.lc[0], L, R);
+                pa[0] = 0.5 * (L + R);
+                da += P.alpha[0] * (R - L);
+                line_lr<S>(wx + SH + 1, P.lc[0], L, R);
+                pb[0] = 0.5 * (L + R);
+                db += P.alpha[0] * (R - L);
             }
-            line_lr<S>(wx + SH, P.lc[0], L, R);
-            pa[0] = 0.5 * (L + R);
-            da += P.alpha[0] * (R - L);
-            line_lr<S>(wx + SH + 1, P.lc[0], L, R);
-            pb[0] = 0.5 * (L + R);
-            db += P.alpha[0] * (R - L);
-            // y: one 128-bit load per row gives both nodes' windows
-            double ya[2 * W + 1], yb[2 * W + 1];
+            double ca, cb;  // centre values
+            {   // y: one 128-bit load per row gives both nodes' windows
+                double wa[2 * W + 1], wb[2 * W + 1];
 #pragma unroll
-            for (int k = -W; k <= W; ++k) {
-                const double2 v = *reinterpret_cast<const double2*>(cur + me_ + k * pitch);
-                ya[W + k] = v.x;
-                yb[W + k] = v.y;
+                for (int k = -W; k <= W; ++k) {
+                    const double2 v = *reinterpret_cast<const double2*>(cur + me + k * pitch);
+                    wa[W + k] = v.x;
+                    wb[W + k] = v.y;
+                }
+                ca = wa[W];
+                cb = wb[W];
+                line_lr<S>(wa, P.lc[1], L, R);
+                pa[1] = 0.5 * (L + R);
+                da += P.alpha[1] * (R - L);
+                line_lr<S>(wb, P.lc[1], L, R);
+                pb[1] = 0.5 * (L + R);
+                db += P.alpha[1] * (R - L);
             }
-            line_lr<S>(ya, P.lc[1], L, R);
-            pa[1] = 0.5 * (L + R);
-            da += P.alpha[1] * (R - L);
-            line_lr<S>(yb, P.lc[1], L, R);
-            pb[1] = 0.5 * (L + R);
-            db += P.alpha[1] * (R - L);
-            // z: register windows
-            line_lr<S>(s0, P.lc[2], L, R);
-            pa[2] = 0.5 * (L + R);
-            da += P.alpha[2] * (R - L);
-            line_lr<S>(s1, P.lc[2], L, R);
-            pb[2] = 0.5 * (L + R);
-            db += P.alpha[2] * (R - L);
+            {   // z: the pair's slot in the 2W+1 resident planes
+                double wa[2 * W + 1], wb[2 * W + 1];
+#pragma unroll
+                for (int k = -W; k <= W; ++k) {
+                    const double2 v = *reinterpret_cast<const double2*>(zpl[W + k]);
+                    wa[W + k] = v.x;
+                    wb[W + k] = v.y;
+                }
+                line_lr<S>(wa, P.lc[2], L, R);
+                pa[2] = 0.5 * (L + R);
+                da += P.alpha[2] * (R - L);
+                line_lr<S>(wb, P.lc[2], L, R);
+                pb[2] = 0.5 * (L + R);
+                db += P.alpha[2] * (R - L);
+            }
+            double b0 = 0.0, b1 = 0.0;
+            if (MODE == MODE_COMBINE) {
+                const double2 v = *reinterpret_cast<const double2*>(vslot(z) + vme);
+                b0 = v.x;
+                b1 = v.y;
+            }
             double xs[3] = {ax0, ay, az};
-            const double oa = finish_node<KIND, MODE>(P, xs, tr, pa, da, s0[W], b0, bad);
+            const double oa = finish_node<KIND, MODE>(P, xs, tr, pa, da, ca, b0, bad);
             xs[0] = ax1;
             bool bad_b = false;
-            const double ob = finish_node<KIND, MODE>(P, xs, tr, pb, db, s1[W], b1, bad_b);
+            const double ob = finish_node<KIND, MODE>(P, xs, tr, pb, db, cb, b1, bad_b);
             P.out[idx] = oa;
             if (two) {
                 P.out[idx + 1] = ob;
@@ -289,19 +347,10 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
                 kmax = max(kmax, max(ka, kb));
             }
         }
-#pragma unroll
-        for (int j = 0; j < 2 * W; ++j) {
-            s0[j] = s0[j + 1];
-            s1[j] = s1[j + 1];
-        }
-        s0[2 * W] = n0v;
-        s1[2 * W] = n1v;
         az = azn;
         tr = trn;
-        b0 = nb0;
-        b1 = nb1;
-        __syncthreads();  // plane z+1 staged; everyone is done reading plane z's buffer
     }
+    cp_async_wait<0>();
 
     if (P.flags && __any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
     if (RANGE && P.range) {

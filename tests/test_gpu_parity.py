@@ -322,3 +322,24 @@ def test_generic_kernel_3d_still_exact(ctx, port, monkeypatch):
     vb, sb, _ = port.integrate(S.grid, S.problem, S.method, 0.0, 0.03, v0)
     assert_bitwise(sa, sb, "steps")
     assert_bitwise(va, vb, "v")
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5", "rotation"])
+def test_weno5_fast_within_tolerance(ctx, port, name):
+    """LSG_OPT_WENO5_FAST (one division per side) stays within the north_star
+    tolerance of the exact reference: 1e-10 relative (inf-norm) on the value
+    function, identical step log (dt does not depend on v)."""
+    S = P.CONFIGS[name](**H.small(name))
+    fast = abi.make_problem(S.problem.kind, abi.SCHEME_WENO5, list(S.problem.params), S.problem.direction,
+                            bool(S.problem.restrict_update), options=abi.OPT_WENO5_FAST)
+    v0 = H.initial_value(port, S)
+    va, sa, ta = ctx.integrate(S.grid, fast, S.method, 0.0, 0.05, v0)
+    vb, sb, tb = port.integrate(S.grid, S.problem, S.method, 0.0, 0.05, v0)
+    assert ta == tb and len(sa) == len(sb)
+    assert_bitwise(sa[:, :3], sb[:, :3], "t, dt, bound")
+    assert rel_inf(va, vb) <= 1e-10, rel_inf(va, vb)
+    assert rel_inf(sa[:, 3:], sb[:, 3:]) <= 1e-10
+    # sign / zero-level-set membership away from ties
+    tie = 1e-9 * np.max(np.abs(vb))
+    away = np.abs(vb) > tie
+    assert np.array_equal(np.sign(va[away]), np.sign(vb[away]))
