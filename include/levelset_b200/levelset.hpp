@@ -30,6 +30,7 @@
 #include <memory>
 #include <set>
 #include <span>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -234,6 +235,27 @@ SolveOutcome solve_brt(const ProblemSetup& setup, std::pair<double, double> tspa
 ScalarField sphere(GridPtr grid, const std::vector<double>& center, double radius);
 ScalarField cylinder(GridPtr grid, const std::set<int>& ignored_dims, const std::vector<double>& center,
                      double radius);
+
+// ---- runner.hpp: convergence study on the device kernels ---------------------------
+struct ConvergenceRow {
+    int n = 0;
+    double dx = 0.0;
+    double max_error = 0.0;
+    double order = 0.0;  // NaN on the coarsest level
+    bool exact = false;  // error at rounding level; order not meaningful
+};
+/// runner.cpp:298-341 with upwind_derivative on the B200 (profile "sin" or "linear").
+std::vector<ConvergenceRow> convergence_study(DerivativeScheme scheme, int refinements,
+                                              const std::string& profile = "sin");
+
+// ---- snapshot.hpp: checkpoint files in the reference format --------------------------
+struct Snapshot {
+    GridPtr grid;
+    ScalarField field;
+    double time = 0.0;
+};
+void write_snapshot(const std::string& path, const ScalarField& field, double time);
+Snapshot read_snapshot(const std::string& path);
 
 // ---- device selection -----------------------------------------------------------------
 /// CUDA device used by this thread's calls (default 0).

@@ -199,6 +199,14 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
                   int* n_out, lsg_steplog* steps, size_t log_cap, size_t* n_steps,
                   double* integration_seconds);
 
+/* ---- checkpoint output in the reference's snapshot format ----------------
+ * snapshot.cpp:69-129: text header "dims/counts/mins/maxs/time" (reals with 17
+ * significant digits) + little-endian fp64 payload in column-major order. */
+int lsg_write_snapshot(const lsg_grid* g, const double* field, double time, const char* path);
+/* Reads the header (periodic_mask is 0: the format does not store boundary tags,
+ * snapshot.hpp:9-11) and, when field != NULL, the payload (cap doubles). */
+int lsg_read_snapshot(const char* path, lsg_grid* g, double* time, double* field, size_t cap);
+
 /* ---- device-resident solver (the fast path bench.py measures) --------------
  * Holds the value function in HBM across steps; in a distributed context it
  * holds this rank's slab of the global grid. */
@@ -233,6 +241,9 @@ int lsg_solver_step_timed(lsg_solver* s, double t, double dt, double* stage_ms, 
 /* run_cfl over [t0, tf] with the reference's step control (integrator.cpp:22-97). */
 int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* opts,
                          lsg_steplog* steps, size_t log_cap, size_t* n_steps, double* t_final);
+/* Snapshot of the resident value function (this rank's slab in a distributed
+ * context, written with the slab's own sub-grid header). */
+int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path);
 /* Raw CUDA stream (cudaStream_t) of the context, for external event timing. */
 int lsg_solver_stream(lsg_solver* s, void** stream);
 /* Kernels one lsg_solver_step launches. */

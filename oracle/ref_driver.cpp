@@ -28,6 +28,8 @@
 #include "levelset/implicit_surfaces.hpp"
 #include "levelset/integrator.hpp"
 #include "levelset/reachability.hpp"
+#include "levelset/runner.hpp"
+#include "levelset/snapshot.hpp"
 #include "levelset/spatial_derivatives.hpp"
 
 #include "../include/lsg.h"
@@ -420,6 +422,47 @@ int ref_bench(const lsg_grid* g, const lsg_problem* p, int method, const double*
             if (!e.empty()) throw std::runtime_error(e);
         *seconds = std::chrono::duration<double>(stop - start).count();
         *steps_per_replica = counts[0];
+    });
+}
+
+// snapshot.cpp:69-129
+int ref_write_snapshot(const lsg_grid* g, const double* field, double time, const char* path) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        write_snapshot(path, ScalarField(grid, std::vector<double>(field, field + grid->node_count())), time);
+    });
+}
+
+int ref_read_snapshot(const char* path, lsg_grid* g, double* time, double* field, std::size_t cap) {
+    return guarded([&] {
+        Snapshot s = read_snapshot(path);
+        lsg_grid out{};
+        out.dim = s.grid->dim();
+        for (int d = 0; d < out.dim && d < LSG_MAX_DIM; ++d) {
+            out.counts[d] = s.grid->count(d);
+            out.mins[d] = s.grid->min(d);
+            out.maxs[d] = s.grid->max(d);
+        }
+        *g = out;
+        *time = s.time;
+        if (field) {
+            if (cap < s.field.size()) throw std::invalid_argument("ref: buffer too small");
+            std::memcpy(field, s.field.values().data(), s.field.size() * sizeof(double));
+        }
+    });
+}
+
+// runner.cpp:298-341: rows of (n, dx, max_error, order)
+int ref_convergence_study(int scheme, int refinements, int periodic, double* rows, int* nrows) {
+    return guarded([&] {
+        auto r = convergence_study(scheme_of(scheme), refinements, periodic ? "sin" : "linear");
+        for (std::size_t k = 0; k < r.size(); ++k) {
+            rows[4 * k + 0] = r[k].n;
+            rows[4 * k + 1] = r[k].dx;
+            rows[4 * k + 2] = r[k].max_error;
+            rows[4 * k + 3] = r[k].order;
+        }
+        *nrows = static_cast<int>(r.size());
     });
 }
 

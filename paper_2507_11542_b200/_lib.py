@@ -24,12 +24,12 @@ EXPORTS = (
     "lsg_ctx_synchronize", "lsg_ctx_launch_count",
     "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis", "lsg_slab_partition",
     "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update",
-    "lsg_integrate", "lsg_solve_brt",
+    "lsg_integrate", "lsg_solve_brt", "lsg_write_snapshot", "lsg_read_snapshot",
     "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
     "lsg_solver_set_field", "lsg_solver_get_field", "lsg_solver_set_field_device",
     "lsg_solver_field_device", "lsg_solver_init_shape", "lsg_solver_step_bound", "lsg_solver_step",
     "lsg_solver_step_timed",
-    "lsg_solver_integrate", "lsg_solver_stream", "lsg_solver_launches_per_step",
+    "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
 )
 
 _lib = None
@@ -253,6 +253,9 @@ class Solver:
              C.byref(opts) if opts is not None else None, log, C.c_size_t(log_cap), C.byref(n), C.byref(tfin))
         return _steps(log, n.value, log_cap), tfin.value
 
+    def write_snapshot(self, time, path):
+        call("lsg_solver_write_snapshot", self.h, C.c_double(time), str(path).encode())
+
     def stream(self):
         p = C.c_void_p()
         call("lsg_solver_stream", self.h, C.byref(p))
@@ -268,6 +271,22 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     call("lsg_nccl_unique_id", buf)
     return bytes(buf)
+
+
+def write_snapshot(g, field, time, path):
+    """snapshot.cpp:69-93 format (host-only)."""
+    field = np.ascontiguousarray(field, dtype=np.float64)
+    call("lsg_write_snapshot", C.byref(g), abi.dptr(field), C.c_double(time), str(path).encode())
+
+
+def read_snapshot(path):
+    """(grid, field, time) from a snapshot.cpp:95-129 file (host-only)."""
+    g = abi.LsgGrid()
+    t = C.c_double()
+    call("lsg_read_snapshot", str(path).encode(), C.byref(g), C.byref(t), None, C.c_size_t(0))
+    out = np.empty(node_count(g), dtype=np.float64)
+    call("lsg_read_snapshot", str(path).encode(), C.byref(g), C.byref(t), abi.dptr(out), C.c_size_t(out.size))
+    return g, out, t.value
 
 
 def slab_partition(n, nranks, rank):

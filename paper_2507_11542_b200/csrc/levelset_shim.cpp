@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <numbers>
 #include <stdexcept>
 #include <string>
 
@@ -440,6 +441,60 @@ SolveOutcome solve_brt(const ProblemSetup& setup, std::pair<double, double> tspa
     out.steps = to_steps(log, std::min(n_steps, log.size()));
     out.integration_seconds = seconds;
     return out;
+}
+
+// ---- runner.cpp:298-341 ---------------------------------------------------------------------
+std::vector<ConvergenceRow> convergence_study(DerivativeScheme scheme, int refinements, const std::string& profile) {
+    if (refinements < 1) throw std::invalid_argument("convergence_study: refinements must be at least 1");
+    if (profile != "sin" && profile != "linear")
+        throw std::invalid_argument("convergence_study: unknown profile '" + profile + "' (valid: sin, linear)");
+    const bool periodic = profile == "sin";
+    constexpr double two_pi = 2.0 * std::numbers::pi;
+    std::vector<ConvergenceRow> rows;
+    for (int level = 0; level <= refinements; ++level) {
+        const int n = 32 << level;
+        GridPtr grid = periodic ? Grid::create({0.0}, {1.0 - 1.0 / static_cast<double>(n)}, {n}, {0})
+                                : Grid::create({0.0}, {1.0}, {n});
+        ScalarField v(grid);
+        for (int i = 0; i < n; ++i) {
+            const double x = grid->axis(0)[static_cast<std::size_t>(i)];
+            v[static_cast<std::size_t>(i)] = periodic ? std::sin(two_pi * x) : x;
+        }
+        const DerivativePair pair = upwind_derivative(v, 0, scheme);  // device
+        double max_error = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double x = grid->axis(0)[static_cast<std::size_t>(i)];
+            const double truth = periodic ? two_pi * std::cos(two_pi * x) : 1.0;
+            max_error = std::max(max_error, std::abs(pair.left[static_cast<std::size_t>(i)] - truth));
+            max_error = std::max(max_error, std::abs(pair.right[static_cast<std::size_t>(i)] - truth));
+        }
+        ConvergenceRow row;
+        row.n = n;
+        row.dx = grid->spacing(0);
+        row.max_error = max_error;
+        row.exact = max_error <= 1e-12;
+        row.order = rows.empty() ? std::numeric_limits<double>::quiet_NaN() : std::log2(rows.back().max_error / max_error);
+        rows.push_back(row);
+    }
+    return rows;
+}
+
+// ---- snapshot.cpp:69-129 ----------------------------------------------------------------------
+void write_snapshot(const std::string& path, const ScalarField& field, double time) {
+    lsg_grid g = to_c(field.grid());
+    check(lsg_write_snapshot(&g, field.values().data(), time, path.c_str()));
+}
+
+Snapshot read_snapshot(const std::string& path) {
+    lsg_grid g{};
+    double t = 0.0;
+    check(lsg_read_snapshot(path.c_str(), &g, &t, nullptr, 0));
+    std::vector<double> mins(g.mins, g.mins + g.dim), maxs(g.maxs, g.maxs + g.dim);
+    std::vector<int> counts(g.counts, g.counts + g.dim);
+    GridPtr grid = Grid::create(mins, maxs, counts);
+    std::vector<double> data(grid->node_count());
+    check(lsg_read_snapshot(path.c_str(), &g, &t, data.data(), data.size()));
+    return Snapshot{grid, ScalarField(grid, std::move(data)), t};
 }
 
 // ---- implicit_surfaces.cpp:20-71 (device generator) ----------------------------------------

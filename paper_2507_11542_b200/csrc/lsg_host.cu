@@ -20,6 +20,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -912,6 +914,82 @@ int lsg_slab_partition(int n, int nranks, int rank, int* z0, int* nz) {
     });
 }
 
+// ---- snapshot I/O (snapshot.cpp:69-129) -------------------------------------
+
+int lsg_write_snapshot(const lsg_grid* g, const double* field, double time, const char* path) {
+    return guarded([&] {
+        check_grid(g);
+        std::ofstream os(path, std::ios::binary);
+        if (!os) fail(LSG_ENUMERIC, std::string("snapshot: cannot open ") + path + " for writing");
+        std::ostringstream h;
+        h.precision(17);
+        h << "dims " << g->dim << "\n" << "counts";
+        for (int d = 0; d < g->dim; ++d) h << " " << g->counts[d];
+        h << "\nmins";
+        for (int d = 0; d < g->dim; ++d) h << " " << g->mins[d];
+        h << "\nmaxs";
+        for (int d = 0; d < g->dim; ++d) h << " " << g->maxs[d];
+        h << "\ntime " << time << "\n";
+        os << h.str();
+        static_assert(sizeof(double) == 8, "fp64");
+        os.write(reinterpret_cast<const char*>(field), static_cast<std::streamsize>(sizeof(double) * node_count(g)));
+        if (!os) fail(LSG_ENUMERIC, std::string("snapshot: write to ") + path + " failed");
+    });
+}
+
+int lsg_read_snapshot(const char* path, lsg_grid* g, double* time, double* field, size_t cap) {
+    return guarded([&] {
+        std::ifstream is(path, std::ios::binary);
+        if (!is) fail(LSG_ENUMERIC, std::string("snapshot: cannot open ") + path);
+        auto line = [&](const std::string& key) {
+            std::string l;
+            if (!std::getline(is, l)) fail(LSG_ENUMERIC, "snapshot: truncated header, expected '" + key + "'");
+            if (l.rfind(key + " ", 0) != 0 && l != key)
+                fail(LSG_ENUMERIC, "snapshot: expected header line '" + key + "', got '" + l + "'");
+            return l.size() > key.size() ? l.substr(key.size() + 1) : std::string();
+        };
+        const int dims = std::stoi(line("dims"));
+        if (dims < 1 || dims > 16) fail(LSG_ENUMERIC, "snapshot: implausible dimension count");
+        if (dims > LSG_MAX_DIM) fail(LSG_EINVAL, "snapshot: the device path supports at most 6 dimensions");
+        lsg_grid out{};
+        out.dim = dims;
+        auto reals = [&](const std::string& key, double* dst, int n) {
+            std::istringstream ss(line(key));
+            int k = 0;
+            double v;
+            while (ss >> v) {
+                if (k < n) dst[k] = v;
+                ++k;
+            }
+            if (k != n) fail(LSG_ENUMERIC, "snapshot: header line '" + key + "' has wrong arity");
+        };
+        {
+            std::istringstream cs(line("counts"));
+            int k = 0, c;
+            while (cs >> c) {
+                if (k < dims) out.counts[k] = c;
+                ++k;
+            }
+            if (k != dims) fail(LSG_ENUMERIC, "snapshot: header line 'counts' has wrong arity");
+        }
+        reals("mins", out.mins, dims);
+        reals("maxs", out.maxs, dims);
+        double t = 0.0;
+        reals("time", &t, 1);
+        check_grid(&out);
+        *g = out;
+        if (time) *time = t;
+        if (field) {
+            const long long N = node_count(&out);
+            if (static_cast<long long>(cap) < N) fail(LSG_EINVAL, "snapshot: output buffer too small");
+            is.read(reinterpret_cast<char*>(field), static_cast<std::streamsize>(sizeof(double) * N));
+            if (!is) fail(LSG_ENUMERIC, std::string("snapshot: payload truncated in ") + path);
+            for (long long i = 0; i < N; ++i)
+                if (!std::isfinite(field[i])) fail(LSG_ENUMERIC, "snapshot: payload contains non-finite values");
+        }
+    });
+}
+
 int lsg_pad_ghost(lsg_ctx* ctx, const lsg_grid* g, const double* field, int dim, int width, double* out) {
     return guarded([&] {
         activate(ctx);
@@ -1244,6 +1322,27 @@ int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* op
         run_cfl(s, t0, tf, opts, log, &tfin);
         copy_log(log, steps, log_cap, n_steps);
         if (t_final) *t_final = tfin;
+    });
+}
+
+int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path) {
+    return guarded([&] {
+        activate(s->ctx);
+        lsg_grid g = s->g;
+        size_t n = static_cast<size_t>(s->total);
+        if (s->distributed) {  // this rank's slab as its own sub-grid
+            const Slab& sl = s->slabs[0];
+            const int D = s->D;
+            const double dz = spacing(&s->g, D - 1);
+            g.counts[D - 1] = sl.nz;
+            g.mins[D - 1] = s->g.mins[D - 1] + static_cast<double>(sl.z0) * dz;
+            g.maxs[D - 1] = s->g.mins[D - 1] + static_cast<double>(sl.z0 + sl.nz - 1) * dz;
+            n = static_cast<size_t>(sl.nodes);
+        }
+        std::vector<double> host(n);
+        download(s, host.data(), s->cur);
+        const int rc = lsg_write_snapshot(&g, host.data(), time, path);
+        if (rc) fail(rc, g_err);
     });
 }
 

@@ -343,3 +343,36 @@ def test_weno5_fast_within_tolerance(ctx, port, name):
     tie = 1e-9 * np.max(np.abs(vb))
     away = np.abs(vb) > tie
     assert np.array_equal(np.sign(va[away]), np.sign(vb[away]))
+
+
+@pytest.mark.parametrize("scheme", [0, 1, 2, 3])
+@pytest.mark.parametrize("profile", ["sin", "linear"])
+def test_convergence_study_matches_reference(ctx, ref, scheme, profile):
+    """runner.cpp:298-341 (acceptance criterion 1) on the device kernels: the
+    table equals the reference's bit for bit and shows the design orders."""
+    import ctypes as C
+    from paper_2507_11542_b200.studies import convergence_study
+
+    rows = convergence_study(ctx, scheme, 3, profile)
+    buf = (C.c_double * 64)()
+    n = C.c_int()
+    assert ref.lib.ref_convergence_study(scheme, 3, 1 if profile == "sin" else 0, buf, C.byref(n)) == 0
+    ref_rows = [tuple(buf[4 * k:4 * k + 4]) for k in range(n.value)]
+    assert len(rows) == len(ref_rows) == 4
+    for a, b in zip(rows, ref_rows):
+        assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2]
+        assert (np.isnan(a[3]) and np.isnan(b[3])) or a[3] == b[3]
+    if profile == "sin":
+        assert rows[-1][3] >= {0: 0.9, 1: 1.8, 2: 2.7, 3: 4.3}[scheme]
+    else:
+        assert rows[-1][2] <= 1e-12
+
+
+def test_solver_snapshot_roundtrip(ctx, port, tmp_path):
+    S = P.cfg2_air3d(21)
+    s = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    s.init_shape(*S.ic[:3], S.ic[3])
+    s.write_snapshot(0.0, tmp_path / "ck.bin")
+    g, v, t = _lib.read_snapshot(tmp_path / "ck.bin")
+    assert t == 0.0 and g.counts[2] == 21
+    assert_bitwise(v, H.initial_value(port, S), "snapshot payload")
