@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "liblsg_b200.so")
 EXPORTS = (
     "lsg_abi_version", "lsg_last_error", "lsg_opts_default", "lsg_device_count",
     "lsg_ctx_create", "lsg_nccl_unique_id", "lsg_ctx_create_dist", "lsg_ctx_destroy",
-    "lsg_ctx_synchronize", "lsg_ctx_launch_count",
+    "lsg_ctx_synchronize", "lsg_ctx_launch_count", "lsg_host_alloc", "lsg_host_free",
     "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis", "lsg_slab_partition",
     "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update",
     "lsg_integrate", "lsg_solve_brt", "lsg_write_snapshot", "lsg_read_snapshot",
@@ -209,8 +209,12 @@ class Solver:
             raise ValueError("field: data size does not match the local node count")
         call("lsg_solver_set_field", self.h, abi.dptr(v))
 
-    def get_field(self):
-        out = np.empty(self.local_nodes, dtype=np.float64)
+    def get_field(self, out=None):
+        """Download the resident field (into `out`, e.g. a pinned buffer, when given)."""
+        if out is None:
+            out = np.empty(self.local_nodes, dtype=np.float64)
+        elif out.dtype != np.float64 or out.size != self.local_nodes or not out.flags.c_contiguous:
+            raise ValueError("get_field: out must be a contiguous float64 array of local_nodes values")
         call("lsg_solver_get_field", self.h, abi.dptr(out))
         return out
 
@@ -271,6 +275,29 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     call("lsg_nccl_unique_id", buf)
     return bytes(buf)
+
+
+class PinnedArray:
+    """float64 numpy view of a page-locked buffer from lsg_host_alloc.
+    Keep this object alive while `array` is in use (freeing it unpins the memory)."""
+
+    def __init__(self, n):
+        p = C.c_void_p()
+        call("lsg_host_alloc", C.c_size_t(8 * max(1, n)), C.byref(p))
+        self.ptr = p
+        self.array = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(n,))
+
+    def free(self):
+        if self.ptr:
+            self.array = None
+            load().lsg_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def write_snapshot(g, field, time, path):

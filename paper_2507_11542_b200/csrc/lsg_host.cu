@@ -879,6 +879,19 @@ int lsg_ctx_launch_count(const lsg_ctx* ctx, uint64_t* count) {
     });
 }
 
+int lsg_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        *out = nullptr;
+        CUDA_CHECK(cudaMallocHost(out, bytes));
+    });
+}
+
+int lsg_host_free(void* p) {
+    return guarded([&] {
+        if (p) CUDA_CHECK(cudaFreeHost(p));
+    });
+}
+
 int lsg_grid_check(const lsg_grid* g) {
     return guarded([&] { check_grid(g); });
 }
