@@ -309,6 +309,13 @@ struct lsg_solver {
     size_t m3_smem = 0;
     std::string invalid;  // deferred invalid_argument (raised at the first term evaluation)
     int cur = 0;
+    cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    ~lsg_solver() {
+        if (ev_ready) cudaEventDestroy(ev_ready);
+        if (ev_halo) cudaEventDestroy(ev_halo);
+        if (comm) cudaStreamDestroy(comm);
+    }
 };
 
 namespace {
@@ -339,6 +346,11 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->total = node_count(g);
     for (int d = 0; d + 1 < s->D; ++d) s->plane *= g->counts[d];
     s->halo_w = s->P > 1 ? s->W : 0;
+    if (s->halo_w) {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaEventCreateWithFlags(&s->ev_ready, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&s->ev_halo, cudaEventDisableTiming));
+    }
     const int nlast = g->counts[s->D - 1];
     if (s->P > nlast) fail(LSG_EINVAL, "slab decomposition: more slabs than planes along the last axis");
 
@@ -545,7 +557,7 @@ void check_alpha_valid(lsg_solver* s) {
 
 // Fill the ghost planes of buffer b: from the neighbour slabs (device copies
 // in-process, NCCL send/recv across ranks); ring for a periodic last axis.
-void exchange(lsg_solver* s, int b) {
+void exchange(lsg_solver* s, int b, cudaStream_t st) {
     if (s->halo_w == 0) return;
     lsg_ctx* ctx = s->ctx;
     const bool periodic = bc_of(&s->g, s->D - 1) == LSG_BC_PERIODIC;
@@ -560,12 +572,11 @@ void exchange(lsg_solver* s, int b) {
             if (lo >= 0) {
                 const Slab& o = s->slabs[lo];
                 CUDA_CHECK(cudaMemcpyAsync(me.f[b] - w * s->plane, o.f[b] + (o.nz - w) * s->plane, bytes,
-                                           cudaMemcpyDeviceToDevice, ctx->stream));
+                                           cudaMemcpyDeviceToDevice, st));
             }
             if (hi >= 0) {
                 const Slab& o = s->slabs[hi];
-                CUDA_CHECK(cudaMemcpyAsync(me.f[b] + me.nz * s->plane, o.f[b], bytes, cudaMemcpyDeviceToDevice,
-                                           ctx->stream));
+                CUDA_CHECK(cudaMemcpyAsync(me.f[b] + me.nz * s->plane, o.f[b], bytes, cudaMemcpyDeviceToDevice, st));
             }
         }
         return;
@@ -578,18 +589,43 @@ void exchange(lsg_solver* s, int b) {
     // Per peer pair the messages match in issue order: every rank first sends
     // up, then down, and receives from below before from above.
     NCCL_CHECK(ncclGroupStart());
-    if (hi >= 0) NCCL_CHECK(ncclSend(me.f[b] + (me.nz - w) * s->plane, cnt, ncclFloat64, hi, ctx->comm, ctx->stream));
-    if (lo >= 0) NCCL_CHECK(ncclSend(me.f[b], cnt, ncclFloat64, lo, ctx->comm, ctx->stream));
-    if (lo >= 0) NCCL_CHECK(ncclRecv(me.f[b] - w * s->plane, cnt, ncclFloat64, lo, ctx->comm, ctx->stream));
-    if (hi >= 0) NCCL_CHECK(ncclRecv(me.f[b] + me.nz * s->plane, cnt, ncclFloat64, hi, ctx->comm, ctx->stream));
+    if (hi >= 0) NCCL_CHECK(ncclSend(me.f[b] + (me.nz - w) * s->plane, cnt, ncclFloat64, hi, ctx->comm, st));
+    if (lo >= 0) NCCL_CHECK(ncclSend(me.f[b], cnt, ncclFloat64, lo, ctx->comm, st));
+    if (lo >= 0) NCCL_CHECK(ncclRecv(me.f[b] - w * s->plane, cnt, ncclFloat64, lo, ctx->comm, st));
+    if (hi >= 0) NCCL_CHECK(ncclRecv(me.f[b] + me.nz * s->plane, cnt, ncclFloat64, hi, ctx->comm, st));
     NCCL_CHECK(ncclGroupEnd());
 }
 
-void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range) {
+// zlo/zhi: plane range [zlo, zhi) of every slab (zhi < 0: up to the slab end,
+// measured from the end when zlo < 0 is not used).
+void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range,
+                  int part = 0) {
     lsg_ctx* ctx = s->ctx;
     const int D = s->D;
     for (Slab& sl : s->slabs) {
+        // part 0: all planes; 1: interior planes [W, nz-W) that need no ghost
+        // planes; 2: the two boundary bands (launched after the exchange)
+        int zlo = 0, zhi = sl.nz;
+        const int W = s->halo_w;
+        if (part == 1) {
+            zlo = W, zhi = sl.nz - W;
+            if (zhi <= zlo) continue;
+        }
+        for (int band = 0; band < (part == 2 ? 2 : 1); ++band) {
+        if (part == 2) {
+            if (sl.nz <= 2 * W) {
+                if (band == 1) break;
+                zlo = 0, zhi = sl.nz;
+            } else if (band == 0) {
+                zlo = 0, zhi = W;
+            } else {
+                zlo = sl.nz - W, zhi = sl.nz;
+            }
+        }
         StageParams P{};
+        P.zlo = zlo;
+        P.zhi = zhi;
+        P.plane = s->plane;
         P.u = sl.f[ui];
         P.v0 = vi >= 0 ? sl.f[vi] : nullptr;
         P.out = sl.f[oi];
@@ -617,16 +653,39 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
         P.flags = s->dflags.as<unsigned>();
         P.range = range;
         if (s->m3fn[mode][0]) {
-            void* args[] = {&P, &sl.m3};
-            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), sl.m3_grid,
+            March3 M = sl.m3;
+            if (zhi - zlo < M.zchunk) M.zchunk = zhi - zlo;
+            const dim3 grid(sl.m3_grid.x, static_cast<unsigned>((zhi - zlo + M.zchunk - 1) / M.zchunk));
+            void* args[] = {&P, &M};
+            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), grid,
                                         dim3(static_cast<unsigned>(s->m3_threads)), args, s->m3_smem, ctx->stream));
         } else {
             void* args[] = {&P};
-            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->fn[mode]),
-                                        dim3((unsigned)((sl.nodes + 255) / 256)), dim3(256), args, 0, ctx->stream));
+            const long long n = static_cast<long long>(zhi - zlo) * s->plane;
+            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->fn[mode]), dim3((unsigned)((n + 255) / 256)),
+                                        dim3(256), args, 0, ctx->stream));
         }
         ctx->note_launch();
+        }
     }
+}
+
+// One fused stage.  With ghost planes (several slabs) the exchange runs on the
+// communication stream while the interior planes are computed; the boundary
+// bands follow once the halos have arrived.
+void run_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range) {
+    if (s->halo_w == 0) {
+        launch_stage(s, mode, ui, vi, oi, dt, c, range, 0);
+        return;
+    }
+    lsg_ctx* ctx = s->ctx;
+    CUDA_CHECK(cudaEventRecord(s->ev_ready, ctx->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s->comm, s->ev_ready, 0));
+    exchange(s, ui, s->comm);
+    CUDA_CHECK(cudaEventRecord(s->ev_halo, s->comm));
+    launch_stage(s, mode, ui, vi, oi, dt, c, range, 1);
+    CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->ev_halo, 0));
+    launch_stage(s, mode, ui, vi, oi, dt, c, range, 2);
 }
 
 // One TVD-RK step (integrator.cpp:58-85); buffers: cur = v, the others scratch.
@@ -640,28 +699,22 @@ void enqueue_step(lsg_solver* s, double dt, unsigned long long* range, cudaEvent
     mark(0);
     if (s->method == LSG_CFL1) {
         const int b = 1 - a;
-        exchange(s, a);
-        launch_stage(s, MODE_EULER, a, -1, b, dt, 0.0, range);
+        run_stage(s, MODE_EULER, a, -1, b, dt, 0.0, range);
         mark(1);
         s->cur = b;
     } else if (s->method == LSG_CFL2) {
         const int b = 1 - a;
-        exchange(s, a);
-        launch_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
+        run_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
         mark(1);
-        exchange(s, b);
-        launch_stage(s, MODE_COMBINE, b, a, a, dt, 0.5, range);
+        run_stage(s, MODE_COMBINE, b, a, a, dt, 0.5, range);
         mark(2);
     } else {
         const int b = (a + 1) % 3, c = (a + 2) % 3;
-        exchange(s, a);
-        launch_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
+        run_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
         mark(1);
-        exchange(s, b);
-        launch_stage(s, MODE_COMBINE, b, a, c, dt, 0.25, nullptr);
+        run_stage(s, MODE_COMBINE, b, a, c, dt, 0.25, nullptr);
         mark(2);
-        exchange(s, c);
-        launch_stage(s, MODE_COMBINE, c, a, a, dt, 2.0 / 3.0, range);
+        run_stage(s, MODE_COMBINE, c, a, a, dt, 2.0 / 3.0, range);
         mark(3);
     }
 }
@@ -1364,7 +1417,12 @@ int lsg_solver_stream(lsg_solver* s, void** stream) {
 }
 
 int lsg_solver_launches_per_step(const lsg_solver* s, int* n) {
-    return guarded([&] { *n = stages_of(s->method) * static_cast<int>(s->slabs.size()); });
+    return guarded([&] {
+        int per_stage = 0;
+        for (const Slab& sl : s->slabs)
+            per_stage += s->halo_w == 0 ? 1 : (sl.nz > 2 * s->halo_w ? 3 : 1);
+        *n = stages_of(s->method) * per_stage;
+    });
 }
 
 }  // extern "C"

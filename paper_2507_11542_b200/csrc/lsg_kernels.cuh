@@ -25,10 +25,10 @@ using StageFn = void (*)(StageParams);
 template <int D, int S, int KIND, int MODE>
 __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ StageParams P) {
     constexpr int W = SchemeWidth<S>::W;
-    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long idx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
-    if (idx < P.n_local) {
+    if (idx < (long long)P.zhi * P.plane) {
         int i[D], ix[D];
         double x[D];
         long long r = idx;

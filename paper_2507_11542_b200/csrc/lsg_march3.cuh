@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
     const int cols = min(TX, n0 - x0), rows = min(M.R, n1 - y0);
-    const int zs = blockIdx.y * M.zchunk;
-    const int ze = min(zs + M.zchunk, P.n[2]);
+    const int zs = P.zlo + blockIdx.y * M.zchunk;
+    const int ze = min(zs + M.zchunk, P.zhi);
     const int yl = t / TX2, pl = t - (t / TX2) * TX2;
     const int xl = 2 * pl;
     const bool active = yl < rows && xl < cols;
