@@ -1,0 +1,103 @@
+// lsg_box3.cuh — one-node-per-thread fused stage kernel for 3-D grids.
+//
+// Block = 256 consecutive nodes of one z-plane's flattened (x, y) index, grid
+// = (plane blocks, planes).  Interior nodes (every window inside the slab)
+// read their three 2W+1 windows straight through the read-only path with
+// constant strides; nodes near a domain edge take the ghost-rule gather
+// (grid.cpp:108-128).  No tile pipeline, no barriers: latency is hidden by
+// occupancy.  Arithmetic identical to stage_kernel (bit-exact).
+#pragma once
+
+#include "lsg_kernels.cuh"
+
+namespace lsg {
+
+template <int S, int KIND, int MODE, bool RANGE>
+__global__ void __launch_bounds__(256) box3_kernel(const __grid_constant__ StageParams P) {
+    constexpr int W = SchemeWidth<S>::W;
+    const int n0 = P.n[0], n1 = P.n[1];
+    const int plane = n0 * n1;
+    const int q = blockIdx.x * 256 + threadIdx.x;
+    const int z = P.zlo + blockIdx.y;
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    bool bad = false;
+    if (q < plane) {
+        const int y = q / n0, x = q - (q / n0) * n0;
+        const long long idx = (long long)z * plane + q;
+        const double* u = P.u + idx;
+        const int zg = P.z0 + z;
+        const bool zin = (zg >= W && zg < P.nz_glob - W) || (P.halo && P.bc[2] == LSG_BC_PERIODIC);
+        double w0[2 * W + 1], w1[2 * W + 1], w2[2 * W + 1];
+        if (x >= W && x < n0 - W && y >= W && y < n1 - W && zin) {
+#pragma unroll
+            for (int k = -W; k <= W; ++k) {
+                w0[W + k] = __ldg(u + k);
+                w1[W + k] = __ldg(u + k * n0);
+                w2[W + k] = __ldg(u + (long long)k * plane);
+            }
+        } else {
+            gather_window<W>(P.u, idx, x, n0, 1, P.bc[0], false, 0, n0, 0, w0);
+            gather_window<W>(P.u, idx, y, n1, n0, P.bc[1], false, 0, n1, 0, w1);
+            gather_window<W>(P.u, idx, z, P.n[2], plane, P.bc[2], true, P.z0, P.nz_glob, P.halo, w2);
+        }
+        double p[3];
+        double diss = 0.0, L, R;
+        line_lr<S>(w0, P.lc[0], L, R);
+        p[0] = 0.5 * (L + R);
+        diss += P.alpha[0] * (R - L);
+        line_lr<S>(w1, P.lc[1], L, R);
+        p[1] = 0.5 * (L + R);
+        diss += P.alpha[1] * (R - L);
+        line_lr<S>(w2, P.lc[2], L, R);
+        p[2] = 0.5 * (L + R);
+        diss += P.alpha[2] * (R - L);
+        const double xs[3] = {__ldg(P.axis[0] + x), __ldg(P.axis[1] + y), __ldg(P.axis[2] + zg)};
+        const double H = hamiltonian<KIND, 3>(P, xs, load_trig<KIND>(P, zg, 0), p);
+        bad = !isfinite(H);
+        double dv = -(H - 0.5 * diss);
+        if (P.restrict_update) dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
+        double o;
+        if constexpr (MODE == MODE_TERM) {
+            o = dv;
+        } else if constexpr (MODE == MODE_EULER) {
+            o = w0[W] + P.dt * dv;
+        } else {
+            const double base = P.v0[idx];
+            o = base + P.c * ((w0[W] + P.dt * dv) - base);
+        }
+        P.out[idx] = o;
+        if (RANGE) kmin = kmax = order_key(o);
+    }
+    if (P.flags && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
+    if (RANGE && P.range) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+        }
+        __shared__ unsigned long long smin[8], smax[8];
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) {
+            smin[warp] = kmin;
+            smax[warp] = kmax;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            kmin = lane < 8 ? smin[lane] : ~0ull;
+            kmax = lane < 8 ? smax[lane] : 0ull;
+#pragma unroll
+            for (int off = 4; off > 0; off >>= 1) {
+                kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+                kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+            }
+            if (lane == 0) {
+                if (kmin != ~0ull) atomicMax(P.range, ~kmin);
+                if (kmax != 0ull) atomicMax(P.range + 1, kmax);
+            }
+        }
+    }
+}
+
+using Box3Fn = void (*)(StageParams);
+
+}  // namespace lsg

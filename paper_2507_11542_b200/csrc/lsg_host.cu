@@ -222,6 +222,21 @@ March3Fn lookup_march3(int kind, int scheme, int mode, bool range) {
     return nullptr;
 }
 
+Box3Fn lookup_box3(int kind, int scheme, int mode, bool range) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return box3_lookup_linear(scheme, mode, range);
+        case LSG_HAM_NORMAL: return box3_lookup_normal(scheme, mode, range);
+        case LSG_HAM_ROCKETS: return box3_lookup_rockets(scheme, mode, range);
+        case LSG_HAM_AIR3D: return box3_lookup_air3d(scheme, mode, range);
+    }
+    return nullptr;
+}
+
+bool kernel_choice(const char* name) {
+    const char* e = std::getenv("LSG_KERNEL");
+    return e && std::string(e) == name;
+}
+
 bool force_generic() {
     const char* e = std::getenv("LSG_KERNEL");
     return e && std::string(e) == "generic";
@@ -303,6 +318,7 @@ struct lsg_solver {
     double bound = 0.0;
     StageFn fn[3] = {nullptr, nullptr, nullptr};
     March3Fn m3fn[3][2] = {};  // [mode][with v-range reduction]
+    Box3Fn b3fn[3][2] = {};
     int m3_threads = 0;
     int m3_pitch = 0;
     int m3_per_sm = 1;
@@ -374,10 +390,14 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             if (!s->fn[m]) s->invalid = "hamiltonian: kind not available for this grid dimension";
         }
 
+    if (s->invalid.empty() && s->D == 3 && kernel_choice("box3") &&
+        static_cast<long long>(g->counts[0]) * g->counts[1] < (1LL << 31))
+        for (int m = 0; m < 3; ++m)
+            for (int r = 0; r < 2; ++r) s->b3fn[m][r] = lookup_box3(p->kind, kscheme, m, r == 1);
     // 2.5-D tiled kernel for 3-D grids (lsg_march3.cuh): TX x R tiles, two
     // x-adjacent nodes per thread, 256 threads per block.
     int TX = 0, R = 0;
-    if (s->invalid.empty() && s->D == 3 && !force_generic()) {
+    if (s->invalid.empty() && s->D == 3 && !force_generic() && !s->b3fn[0][0]) {
         const int n0 = g->counts[0], n1 = g->counts[1];
         if (n0 <= 256) {
             TX = (n0 + 1) & ~1;  // full rows
@@ -652,7 +672,13 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
         std::memcpy(P.hp, s->p.params, sizeof P.hp);
         P.flags = s->dflags.as<unsigned>();
         P.range = range;
-        if (s->m3fn[mode][0]) {
+        if (s->b3fn[mode][0]) {
+            void* args[] = {&P};
+            const long long pl = s->plane;
+            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->b3fn[mode][range ? 1 : 0]),
+                                        dim3(static_cast<unsigned>((pl + 255) / 256), static_cast<unsigned>(zhi - zlo)),
+                                        dim3(256), args, 0, ctx->stream));
+        } else if (s->m3fn[mode][0]) {
             March3 M = sl.m3;
             if (zhi - zlo < M.zchunk) M.zchunk = zhi - zlo;
             const dim3 grid(sl.m3_grid.x, static_cast<unsigned>((zhi - zlo + M.zchunk - 1) / M.zchunk));

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include "lsg_box3.cuh"
 #include "lsg_march3.cuh"
 
 namespace lsg {
@@ -22,6 +23,10 @@ struct ShapeParams {
 
 using AlphaFn = void (*)(AlphaParams);
 
+Box3Fn box3_lookup_linear(int s, int m, bool range);
+Box3Fn box3_lookup_normal(int s, int m, bool range);
+Box3Fn box3_lookup_rockets(int s, int m, bool range);
+Box3Fn box3_lookup_air3d(int s, int m, bool range);
 March3Fn march3_lookup_linear(int s, int m, bool range);
 March3Fn march3_lookup_normal(int s, int m, bool range);
 March3Fn march3_lookup_rockets(int s, int m, bool range);
