@@ -148,29 +148,40 @@ class Context:
              abi.dptr(out))
         return out
 
-    def integrate(self, g, p, method, t0, tf, v0, opts=None, log_cap=1 << 16):
+    def integrate(self, g, p, method, t0, tf, v0, opts=None, log_cap=4096):
         v = np.array(v0, dtype=np.float64, copy=True)
-        log = (abi.LsgStepLog * log_cap)()
         n = C.c_size_t()
         tfin = C.c_double()
-        call("lsg_integrate", self.h, C.byref(g), C.byref(p), C.c_int(method), C.c_double(t0), C.c_double(tf),
-             abi.dptr(v), C.byref(opts) if opts is not None else None, log, C.c_size_t(log_cap), C.byref(n),
-             C.byref(tfin))
-        return v, _steps(log, n.value, log_cap), tfin.value
+        while True:  # LSG_ERANGE reports the log size a leg needs before anything runs
+            log = (abi.LsgStepLog * log_cap)()
+            rc = load().lsg_integrate(self.h, C.byref(g), C.byref(p), C.c_int(method), C.c_double(t0),
+                                      C.c_double(tf), abi.dptr(v), C.byref(opts) if opts is not None else None, log,
+                                      C.c_size_t(log_cap), C.byref(n), C.byref(tfin))
+            if rc == abi.ERANGE and n.value > log_cap:
+                log_cap = n.value
+                continue
+            raise_for(rc)
+            return v, _steps(log, n.value, log_cap), tfin.value
 
-    def solve_brt(self, g, p, v0, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=1 << 16):
+    def solve_brt(self, g, p, v0, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=4096):
         v0 = np.ascontiguousarray(v0, dtype=np.float64)
         N = node_count(g)
         ck = np.empty(max(1, n_checkpoints) * N, dtype=np.float64)
         times = np.empty(max(1, n_checkpoints), dtype=np.float64)
         n_out = C.c_int()
-        log = (abi.LsgStepLog * log_cap)()
         n = C.c_size_t()
         secs = C.c_double()
-        call("lsg_solve_brt", self.h, C.byref(g), C.byref(p), abi.dptr(v0), C.c_double(tspan[0]),
-             C.c_double(tspan[1]), C.c_int(n_checkpoints), C.c_int(method),
-             C.byref(opts) if opts is not None else None, abi.dptr(ck), abi.dptr(times), C.byref(n_out), log,
-             C.c_size_t(log_cap), C.byref(n), C.byref(secs))
+        while True:
+            log = (abi.LsgStepLog * log_cap)()
+            rc = load().lsg_solve_brt(self.h, C.byref(g), C.byref(p), abi.dptr(v0), C.c_double(tspan[0]),
+                                      C.c_double(tspan[1]), C.c_int(n_checkpoints), C.c_int(method),
+                                      C.byref(opts) if opts is not None else None, abi.dptr(ck), abi.dptr(times),
+                                      C.byref(n_out), log, C.c_size_t(log_cap), C.byref(n), C.byref(secs))
+            if rc == abi.ERANGE and n.value > log_cap:
+                log_cap = n.value
+                continue
+            raise_for(rc)
+            break
         k = n_out.value
         return ck[: k * N].reshape(k, N), times[:k].copy(), _steps(log, n.value, log_cap), secs.value
 
@@ -249,13 +260,19 @@ class Solver:
         call("lsg_solver_step_timed", self.h, C.c_double(t), C.c_double(dt), stage, C.byref(total))
         return [stage[k] for k in range(self.method + 1)], total.value
 
-    def integrate(self, t0, tf, opts=None, log_cap=1 << 16):
-        log = (abi.LsgStepLog * log_cap)()
+    def integrate(self, t0, tf, opts=None, log_cap=4096):
         n = C.c_size_t()
         tfin = C.c_double()
-        call("lsg_solver_integrate", self.h, C.c_double(t0), C.c_double(tf),
-             C.byref(opts) if opts is not None else None, log, C.c_size_t(log_cap), C.byref(n), C.byref(tfin))
-        return _steps(log, n.value, log_cap), tfin.value
+        while True:
+            log = (abi.LsgStepLog * log_cap)()
+            rc = load().lsg_solver_integrate(self.h, C.c_double(t0), C.c_double(tf),
+                                             C.byref(opts) if opts is not None else None, log, C.c_size_t(log_cap),
+                                             C.byref(n), C.byref(tfin))
+            if rc == abi.ERANGE and n.value > log_cap:
+                log_cap = n.value
+                continue
+            raise_for(rc)
+            return _steps(log, n.value, log_cap), tfin.value
 
     def write_snapshot(self, time, path):
         call("lsg_solver_write_snapshot", self.h, C.c_double(time), str(path).encode())

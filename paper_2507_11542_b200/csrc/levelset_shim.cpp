@@ -334,14 +334,15 @@ IntegrationResult integrate(TimeIntegrator method, const TermFn& term, std::pair
     lsg_problem p = to_c(problem);
     OptsC o(opts);
     IntegrationResult r{tspan.first, std::move(v0), {}};
-    std::vector<lsg_steplog> log(1u << 16);
+    std::vector<lsg_steplog> log(4096);
     std::size_t n = 0;
     double tfin = tspan.first;
     int rc = lsg_integrate(ctx(), &g, &p, static_cast<int>(method), tspan.first, tspan.second, r.v.values().data(),
                            &o.o, log.data(), log.size(), &n, &tfin);
-    if (rc == LSG_OK && n > log.size()) {  // very long spans: rerun with room for the whole log
+    if (rc == LSG_ERANGE && n > log.size()) {  // the leg needs a longer log: nothing ran, retry
         log.resize(n);
-        throw std::runtime_error("integrate: step log overflow");
+        rc = lsg_integrate(ctx(), &g, &p, static_cast<int>(method), tspan.first, tspan.second, r.v.values().data(),
+                           &o.o, log.data(), log.size(), &n, &tfin);
     }
     check(rc);
     r.t = tfin;
@@ -425,14 +426,22 @@ SolveOutcome solve_brt(const ProblemSetup& setup, std::pair<double, double> tspa
     const std::size_t N = grid->node_count();
     std::vector<double> ck(N * static_cast<std::size_t>(n_checkpoints));
     std::vector<double> times(static_cast<std::size_t>(n_checkpoints));
-    std::vector<lsg_steplog> log(1u << 16);
+    std::vector<lsg_steplog> log(4096);
     int n_out = 0;
     std::size_t n_steps = 0;
     double seconds = 0.0;
     OptsC o(opts);
-    check(lsg_solve_brt(ctx(), &g, &p, setup.initial_value.values().data(), tspan.first, tspan.second, n_checkpoints,
-                        static_cast<int>(method), &o.o, ck.data(), times.data(), &n_out, log.data(), log.size(),
-                        &n_steps, &seconds));
+    auto call = [&] {
+        return lsg_solve_brt(ctx(), &g, &p, setup.initial_value.values().data(), tspan.first, tspan.second,
+                             n_checkpoints, static_cast<int>(method), &o.o, ck.data(), times.data(), &n_out,
+                             log.data(), log.size(), &n_steps, &seconds);
+    };
+    int rc = call();
+    if (rc == LSG_ERANGE && n_steps > log.size()) {  // nothing ran: retry with room for every step
+        log.resize(n_steps);
+        rc = call();
+    }
+    check(rc);
     for (int k = 0; k < n_out; ++k) {
         out.checkpoints.emplace_back(grid, std::vector<double>(ck.begin() + static_cast<std::ptrdiff_t>(k * N),
                                                                 ck.begin() + static_cast<std::ptrdiff_t>((k + 1) * N)));

@@ -373,8 +373,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     // kind / dimension / stencil-room checks are deferred to the first term
     // evaluation, where the reference raises them (reachability.cpp:22,
     // spatial_derivatives.cpp:40-47).
-    if (lookup_stage(p->kind, 1, 0, 0) == nullptr && lookup_stage(p->kind, s->D, 0, 0) == nullptr &&
-        lookup_alpha(p->kind) == nullptr)
+    if (lookup_alpha(p->kind) == nullptr)  // not a device Hamiltonian kind
         s->invalid = "term_lax_friedrichs: problem must provide ham_func and dissipation_bounds";
     else if (kind_dim(p->kind) && kind_dim(p->kind) != s->D)
         s->invalid = "hamiltonian: grid dimension does not match the problem kind";
@@ -768,23 +767,28 @@ lsg_opts default_opts() {
 
 double smin(double a, double b) { return (b < a) ? b : a; }  // std::min
 
-// run_cfl (integrator.cpp:22-97) over the device-resident field.
-void run_cfl(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in, std::vector<lsg_steplog>& log,
-             double* t_final) {
+// The dt schedule of one leg of run_cfl (integrator.cpp:22-97), host only:
+// alpha and the CFL bound are v-independent, so every step's (t, dt) follows
+// from (t0, tf, options) alone.  Validation errors are raised in the
+// reference's order.
+struct LegPlan {
+    std::vector<lsg_steplog> log;
+    double t_final = 0.0;
+    bool collapsed = false;
+};
+
+LegPlan plan_leg(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in) {
     const lsg_opts o = opts_in ? *opts_in : default_opts();
     check_options(&o);
     if (!std::isfinite(t0) || !std::isfinite(tf)) fail(LSG_EINVAL, "integrator: tspan must be finite");
     if (tf < t0) fail(LSG_EINVAL, "integrator: tspan must not be decreasing");
-    log.clear();
-    *t_final = t0;
-    if (tf == t0) return;
+    LegPlan plan;
+    plan.t_final = t0;
+    if (tf == t0) return plan;
     const double eps_stop = o.termination_epsilon * std::abs(tf);
     double t = t0;
-    if (!(tf - t > 0.0 && tf - t >= eps_stop)) return;
+    if (!(tf - t > 0.0 && tf - t >= eps_stop)) return plan;
     check_alpha_valid(s);  // the first term evaluation validates the bounds
-
-    // the dt schedule of the leg (alpha and the bound are v-independent)
-    bool collapsed = false;
     while (tf - t > 0.0 && tf - t >= eps_stop) {
         double target = tf;
         if (o.n_checkpoint_times) {
@@ -797,13 +801,23 @@ void run_cfl(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in, std::
         double dt = smin(remaining, o.max_step);
         dt = smin(dt, o.cfl_factor * s->bound);
         if (!(dt > 0.0)) {
-            collapsed = true;
+            plan.collapsed = true;
             break;
         }
         const bool lands = dt == remaining;
-        log.push_back({t, dt, s->bound, 0.0, 0.0});
+        plan.log.push_back({t, dt, s->bound, 0.0, 0.0});
         t = lands ? target : t + dt;
     }
+    plan.t_final = t;
+    return plan;
+}
+
+// Run a planned leg on the device-resident field: every stage of every step
+// enqueued back to back, one synchronisation at the end for the per-step v
+// range and the error flags.
+void run_leg(lsg_solver* s, LegPlan& plan) {
+    std::vector<lsg_steplog>& log = plan.log;
+    const bool collapsed = plan.collapsed;
     const long long nsteps = static_cast<long long>(log.size());
     lsg_ctx* ctx = s->ctx;
     CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
@@ -829,7 +843,16 @@ void run_cfl(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in, std::
         log[k].v_min = key_to_double(~keys[2 * k]);
         log[k].v_max = key_to_double(keys[2 * k + 1]);
     }
-    *t_final = t;
+}
+
+// Step-log capacity check before any device work: LSG_ERANGE with the needed
+// entry count in *n_steps, nothing modified (the caller retries).
+void check_log_room(size_t need, const lsg_steplog* steps, size_t cap, size_t* n_steps) {
+    if (steps && need > cap) {
+        if (n_steps) *n_steps = need;
+        fail(LSG_ERANGE, "step log capacity " + std::to_string(cap) + " too small: " + std::to_string(need) +
+                             " entries needed");
+    }
 }
 
 void copy_log(const std::vector<lsg_steplog>& log, lsg_steplog* out, size_t cap, size_t* n) {
@@ -1203,13 +1226,13 @@ int lsg_integrate(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int met
     return guarded([&] {
         if (opts) check_options(opts);
         auto s = make_solver(ctx, g, p, method, 1);
+        LegPlan plan = plan_leg(s.get(), t0, tf, opts);
+        check_log_room(plan.log.size(), steps, log_cap, n_steps);
         upload(s.get(), v, 0);
-        std::vector<lsg_steplog> log;
-        double tfin = t0;
-        run_cfl(s.get(), t0, tf, opts, log, &tfin);
+        run_leg(s.get(), plan);
         download(s.get(), v, s->cur);
-        copy_log(log, steps, log_cap, n_steps);
-        if (t_final) *t_final = tfin;
+        copy_log(plan.log, steps, log_cap, n_steps);
+        if (t_final) *t_final = plan.t_final;
     });
 }
 
@@ -1232,17 +1255,27 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
         if (integration_seconds) *integration_seconds = 0.0;
         if (duration == 0.0 || n_checkpoints == 1) return;
         auto s = make_solver(ctx, g, p, method, 1);
-        upload(s.get(), v0, 0);
         const int segments = n_checkpoints - 1;
-        std::vector<lsg_steplog> all, leg;
-        const auto start = std::chrono::steady_clock::now();
+        // every leg's schedule up front (reachability.cpp:160-170: the next leg
+        // starts from leg.t), so the log capacity is known before device work
+        std::vector<LegPlan> plans;
+        size_t total = 0;
         double t = 0.0;
         for (int k = 1; k <= segments; ++k) {
             const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
-            double leg_t = t;
-            run_cfl(s.get(), t, t_end, opts, leg, &leg_t);
-            t = leg_t;
-            all.insert(all.end(), leg.begin(), leg.end());
+            plans.push_back(plan_leg(s.get(), t, t_end, opts));
+            t = plans.back().t_final;
+            total += plans.back().log.size();
+            if (plans.back().collapsed) break;
+        }
+        check_log_room(total, steps, log_cap, n_steps);
+        upload(s.get(), v0, 0);
+        std::vector<lsg_steplog> all;
+        const auto start = std::chrono::steady_clock::now();
+        for (int k = 1; k <= static_cast<int>(plans.size()); ++k) {
+            const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
+            run_leg(s.get(), plans[k - 1]);
+            all.insert(all.end(), plans[k - 1].log.begin(), plans[k - 1].log.end());
             download(s.get(), checkpoints + static_cast<long long>(k) * N, s->cur);
             checkpoint_times[k] = t_end;
             *n_out = k + 1;
@@ -1409,11 +1442,11 @@ int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* op
                          size_t log_cap, size_t* n_steps, double* t_final) {
     return guarded([&] {
         activate(s->ctx);
-        std::vector<lsg_steplog> log;
-        double tfin = t0;
-        run_cfl(s, t0, tf, opts, log, &tfin);
-        copy_log(log, steps, log_cap, n_steps);
-        if (t_final) *t_final = tfin;
+        LegPlan plan = plan_leg(s, t0, tf, opts);
+        check_log_room(plan.log.size(), steps, log_cap, n_steps);
+        run_leg(s, plan);
+        copy_log(plan.log, steps, log_cap, n_steps);
+        if (t_final) *t_final = plan.t_final;
     });
 }
 

@@ -396,3 +396,19 @@ def test_cfg3_full_size_slabs(ctx):
     three.step(0.0, dt)
     assert_bitwise(three.get_field(), a, "3 slabs vs 1 at 81^4")
     assert np.all(np.isfinite(a)) and np.all(a <= v0)  # Grow clamp: values only decrease
+
+
+def test_step_log_capacity_retry(ctx, port):
+    """A leg longer than the caller's step log is reported (LSG_ERANGE with the
+    needed size) before anything runs; the bindings retry transparently."""
+    S = P.cfg1_circle(41)
+    v0 = H.initial_value(port, S)
+    a = ctx.integrate(S.grid, S.problem, S.method, 0.0, 0.2, v0, log_cap=3)
+    b = port.integrate(S.grid, S.problem, S.method, 0.0, 0.2, v0)
+    assert len(a[1]) == len(b[1]) > 3
+    assert_bitwise(a[0], b[0], "v")
+    assert_bitwise(a[1], b[1], "steps")
+    ck, times, steps, _ = ctx.solve_brt(S.grid, S.problem, v0, (0.0, 0.2), 3, S.method, log_cap=2)
+    rk, rt, rs = port.solve_brt(S.grid, S.problem, v0, (0.0, 0.2), 3, S.method)
+    assert_bitwise(ck, rk, "checkpoints")
+    assert_bitwise(steps, rs, "steps")
