@@ -151,6 +151,11 @@ int lsg_ctx_synchronize(lsg_ctx* ctx);
 /* Number of device kernels this context has launched so far. */
 int lsg_ctx_launch_count(const lsg_ctx* ctx, uint64_t* count);
 
+/* Page-locked host buffers for the host<->device copies of the reference-facing
+ * calls (allocated by this library's CUDA runtime). */
+int lsg_host_alloc(size_t bytes, void** out);
+int lsg_host_free(void* p);
+
 /* ---- grid (grid.cpp:9-66, :69-91) ---------------------------------------- */
 /* Validates like Grid::create (grid.cpp:13-26). */
 int lsg_grid_check(const lsg_grid* g);
