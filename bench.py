@@ -123,15 +123,19 @@ def dist_env():
     return ws, rank, local
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_summary():
+    """Per-launch numbers of the dominant kernel from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+            return json.load(f)
     except Exception:
-        return None
+        return {}
+
+
+# FP64 DADD/DMUL issue rate of one B200 (tools/fp64_peak.cu, measured under gpurun):
+# 18.5 T instructions/s = 64 per SM per clock at 1.965 GHz.
+FP64_PEAK = 18.5e12
 
 
 def cpu_reference_sample(setup, v0, seconds_target=10.0, nthreads=1):
@@ -282,7 +286,8 @@ def b200_arm(args):
     comb_bytes = BYTES_STAGE[1] * nodes_local
     peak, peak_kind = peaks()
     achieved = comb_bytes / (comb_ms * 1e-3) / 1e9
-    traffic = ncu_traffic()
+    prof = ncu_summary()
+    traffic = prof.get("dram_bytes_per_launch")
 
     # ---- e2e: public C ABI with pinned host buffers ------------------------
     pinned = _lib.PinnedArray(nodes_local)  # page-locked by the library's own CUDA runtime
@@ -355,6 +360,16 @@ def b200_arm(args):
             "algorithmic_bytes_per_launch": comb_bytes,
             "avg_launch_ms": comb_ms,
             "step_gbs": BYTES_PER_PT_STAGE_RK3 * value / 1e9,
+        },
+        "roofline_fp64": {
+            "bound": "fp64",
+            "achieved": prof.get("fp64_instr_per_node", float("nan")) * nodes_local / (comb_ms * 1e-3),
+            "peak": FP64_PEAK,
+            "unit": "FP64 instr/s",
+            "frac": prof.get("fp64_instr_per_node", float("nan")) * nodes_local / (comb_ms * 1e-3) / FP64_PEAK,
+            "instr_per_node": prof.get("fp64_instr_per_node"),
+            "source": "instr/node from ncu smsp__inst_executed_pipe_fp64.sum (profiles/ncu_summary.json); "
+                      "peak from tools/fp64_peak.cu",
         },
         "e2e": {
             "value": e2e_value,
