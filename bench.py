@@ -350,7 +350,7 @@ def b200_arm(args):
         "gpu_launches": launches,
         "roofline": {
             "bound": "hbm",
-            "kernel": "stage_kernel<3,ENO3,AIR3D,COMBINE>",
+            "kernel": "march3_kernel<ENO3,AIR3D,COMBINE> (2.5-D tiled fused stage)",
             "achieved": achieved,
             "peak": peak,
             "unit": "GB/s",
