@@ -248,6 +248,22 @@ struct ConvergenceRow {
 std::vector<ConvergenceRow> convergence_study(DerivativeScheme scheme, int refinements,
                                               const std::string& profile = "sin");
 
+// ---- contour.hpp: zero-level-set extraction on the device ----------------------------
+struct Point2 {
+    double x = 0.0;
+    double y = 0.0;
+};
+struct Segment2 {
+    Point2 a;
+    Point2 b;
+};
+/// contour.cpp:27-97 — marching squares on the B200, same segments in the same order.
+std::vector<Segment2> extract_zero_set_2d(const ScalarField& field);
+/// contour.cpp:99-135 — 2-D slice of a 3-D field (device gather).
+ScalarField slice_2d(const ScalarField& field, int fixed_dim, int index);
+/// contour.cpp:137-142 — total length (host sum of std::hypot over the segments).
+double polyline_length(const std::vector<Segment2>& segments);
+
 // ---- snapshot.hpp: checkpoint files in the reference format --------------------------
 struct Snapshot {
     GridPtr grid;

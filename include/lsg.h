@@ -212,6 +212,16 @@ int lsg_write_snapshot(const lsg_grid* g, const double* field, double time, cons
  * snapshot.hpp:9-11) and, when field != NULL, the payload (cap doubles). */
 int lsg_read_snapshot(const char* path, lsg_grid* g, double* time, double* field, size_t cap);
 
+/* ---- zero-level-set extraction (contour.cpp:27-135) --------------------------
+ * Marching squares on a 2-D field: segments as {ax, ay, bx, by} quadruples in
+ * the reference's order and arithmetic.  *n_segments receives the total; when
+ * it exceeds cap, nothing is written and LSG_ERANGE is returned.
+ * lsg_slice_2d restricts a 3-D field to fixed_dim = index (out: the 2-D slice,
+ * column-major over the remaining dimensions). */
+int lsg_extract_zero_set_2d(lsg_ctx* ctx, const lsg_grid* g, const double* field, double* segments, size_t cap,
+                            size_t* n_segments);
+int lsg_slice_2d(lsg_ctx* ctx, const lsg_grid* g, const double* field, int fixed_dim, int index, double* out);
+
 /* ---- device-resident solver (the fast path bench.py measures) --------------
  * Holds the value function in HBM across steps; in a distributed context it
  * holds this rank's slab of the global grid. */

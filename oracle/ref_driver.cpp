@@ -23,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "levelset/contour.hpp"
 #include "levelset/grid.hpp"
 #include "levelset/hamiltonian.hpp"
 #include "levelset/implicit_surfaces.hpp"
@@ -449,6 +450,28 @@ int ref_read_snapshot(const char* path, lsg_grid* g, double* time, double* field
             if (cap < s.field.size()) throw std::invalid_argument("ref: buffer too small");
             std::memcpy(field, s.field.values().data(), s.field.size() * sizeof(double));
         }
+    });
+}
+
+// contour.cpp:27-142
+int ref_extract_zero_set_2d(const lsg_grid* g, const double* field, double* segs, std::size_t cap, std::size_t* n,
+                            double* length) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        auto s = extract_zero_set_2d(ScalarField(grid, std::vector<double>(field, field + grid->node_count())));
+        *n = s.size();
+        for (std::size_t k = 0; k < s.size() && k < cap; ++k) {
+            segs[4 * k] = s[k].a.x, segs[4 * k + 1] = s[k].a.y, segs[4 * k + 2] = s[k].b.x, segs[4 * k + 3] = s[k].b.y;
+        }
+        *length = polyline_length(s);
+    });
+}
+
+int ref_slice_2d(const lsg_grid* g, const double* field, int fixed_dim, int index, double* out) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        ScalarField sl = slice_2d(ScalarField(grid, std::vector<double>(field, field + grid->node_count())), fixed_dim, index);
+        std::memcpy(out, sl.values().data(), sl.size() * sizeof(double));
     });
 }
 

@@ -25,6 +25,7 @@ EXPORTS = (
     "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis", "lsg_slab_partition",
     "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update",
     "lsg_integrate", "lsg_solve_brt", "lsg_write_snapshot", "lsg_read_snapshot",
+    "lsg_extract_zero_set_2d", "lsg_slice_2d",
     "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
     "lsg_solver_set_field", "lsg_solver_get_field", "lsg_solver_set_field_device",
     "lsg_solver_field_device", "lsg_solver_init_shape", "lsg_solver_step_bound", "lsg_solver_step",
@@ -184,6 +185,30 @@ class Context:
             break
         k = n_out.value
         return ck[: k * N].reshape(k, N), times[:k].copy(), _steps(log, n.value, log_cap), secs.value
+
+
+    def extract_zero_set_2d(self, g, field):
+        """Marching-squares zero contour (contour.cpp:27-97): array (n, 4) of ax, ay, bx, by."""
+        field = np.ascontiguousarray(field, dtype=np.float64)
+        n = C.c_size_t()
+        cap = 4096
+        while True:
+            seg = np.empty((cap, 4), dtype=np.float64)
+            rc = load().lsg_extract_zero_set_2d(self.h, C.byref(g), abi.dptr(field), abi.dptr(seg), C.c_size_t(cap),
+                                                C.byref(n))
+            if rc == abi.ERANGE and n.value > cap:
+                cap = n.value
+                continue
+            raise_for(rc)
+            return seg[: n.value].copy()
+
+    def slice_2d(self, g, field, fixed_dim, index):
+        """contour.cpp:99-135: the 2-D slice fixed_dim = index of a 3-D field."""
+        field = np.ascontiguousarray(field, dtype=np.float64)
+        kept = [d for d in range(g.dim) if d != fixed_dim]
+        out = np.empty(g.counts[kept[0]] * g.counts[kept[1]] if len(kept) == 2 else 1, dtype=np.float64)
+        call("lsg_slice_2d", self.h, C.byref(g), abi.dptr(field), C.c_int(fixed_dim), C.c_int(index), abi.dptr(out))
+        return out
 
 
 class Solver:

@@ -488,6 +488,49 @@ std::vector<ConvergenceRow> convergence_study(DerivativeScheme scheme, int refin
     return rows;
 }
 
+// ---- contour.cpp:27-142 -----------------------------------------------------------------------
+std::vector<Segment2> extract_zero_set_2d(const ScalarField& field) {
+    lsg_grid g = to_c(field.grid());
+    std::vector<double> seg(4 * 4096);
+    std::size_t n = 0;
+    int rc = lsg_extract_zero_set_2d(ctx(), &g, field.values().data(), seg.data(), seg.size() / 4, &n);
+    if (rc == LSG_ERANGE && n > seg.size() / 4) {
+        seg.resize(4 * n);
+        rc = lsg_extract_zero_set_2d(ctx(), &g, field.values().data(), seg.data(), n, &n);
+    }
+    check(rc);
+    std::vector<Segment2> out(n);
+    for (std::size_t k = 0; k < n; ++k) out[k] = {{seg[4 * k], seg[4 * k + 1]}, {seg[4 * k + 2], seg[4 * k + 3]}};
+    return out;
+}
+
+ScalarField slice_2d(const ScalarField& field, int fixed_dim, int index) {
+    const Grid& g = field.grid();
+    lsg_grid c = to_c(g);
+    if (g.dim() < 3) throw std::invalid_argument("slice_2d: field must be at least 3-D");
+    if (fixed_dim < 0 || fixed_dim >= g.dim()) throw std::invalid_argument("slice_2d: fixed dimension out of range");
+    std::vector<double> mins, maxs;
+    std::vector<int> counts;
+    std::set<int> periodic;
+    for (int d = 0; d < g.dim(); ++d) {
+        if (d == fixed_dim) continue;
+        if (g.boundary(d) == BoundaryCondition::Periodic) periodic.insert(static_cast<int>(counts.size()));
+        mins.push_back(g.min(d));
+        maxs.push_back(g.max(d));
+        counts.push_back(g.count(d));
+    }
+    GridPtr sg = Grid::create(mins, maxs, counts, periodic);
+    ScalarField out(sg);
+    check(lsg_slice_2d(ctx(), &c, field.values().data(), fixed_dim, index, out.values().data()));
+    return out;
+}
+
+double polyline_length(const std::vector<Segment2>& segments) {
+    double length = 0.0;
+    for (const auto& s : segments) length += std::hypot(s.b.x - s.a.x, s.b.y - s.a.y);
+    return length;
+}
+
 // ---- snapshot.cpp:69-129 ----------------------------------------------------------------------
 void write_snapshot(const std::string& path, const ScalarField& field, double time) {
     lsg_grid g = to_c(field.grid());

@@ -1105,6 +1105,67 @@ int lsg_read_snapshot(const char* path, lsg_grid* g, double* time, double* field
     });
 }
 
+int lsg_extract_zero_set_2d(lsg_ctx* ctx, const lsg_grid* g, const double* field, double* segments, size_t cap,
+                            size_t* n_segments) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        if (g->dim != 2) fail(LSG_EINVAL, "extract_zero_set_2d: field must be 2-D");  // contour.cpp:29-30
+        const int nx = g->counts[0], ny = g->counts[1];
+        const long long N = node_count(g);
+        const int ncells = (nx - 1) * (ny - 1);
+        double* df = ctx->staging(0, sizeof(double) * N);
+        std::vector<double> axes(static_cast<size_t>(nx + ny));
+        for (int i = 0; i < nx; ++i) axes[i] = g->mins[0] + static_cast<double>(i) * spacing(g, 0);
+        for (int j = 0; j < ny; ++j) axes[nx + j] = g->mins[1] + static_cast<double>(j) * spacing(g, 1);
+        double* dax = ctx->staging(1, sizeof(double) * axes.size());
+        const size_t tb = zero_set_temp_bytes(ncells);
+        // counts | offsets | cub temp in one staging buffer
+        const size_t ib = (sizeof(int) * static_cast<size_t>(ncells) + 255) & ~size_t(255);
+        char* scratch = reinterpret_cast<char*>(ctx->staging(2, 2 * ib + tb + 256));
+        CUDA_CHECK(cudaMemcpyAsync(df, field, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_CHECK(cudaMemcpyAsync(dax, axes.data(), sizeof(double) * axes.size(), cudaMemcpyHostToDevice, ctx->stream));
+        const long long cap_dev = static_cast<long long>(cap);
+        double* dseg = cap ? ctx->staging(3, sizeof(double) * 4 * cap) : nullptr;
+        int total = 0;
+        zero_set_2d(df, nx, ny, dax, dax + nx, spacing(g, 0), spacing(g, 1), dseg, cap_dev,
+                    reinterpret_cast<int*>(scratch), reinterpret_cast<int*>(scratch + ib), scratch + 2 * ib, tb,
+                    ctx->stream, &total);
+        ctx->note_launch(3);
+        if (n_segments) *n_segments = static_cast<size_t>(total);
+        if (static_cast<size_t>(total) > cap) fail(LSG_ERANGE, "extract_zero_set_2d: segment buffer too small");
+        if (total)
+            CUDA_CHECK(cudaMemcpyAsync(segments, dseg, sizeof(double) * 4 * total, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int lsg_slice_2d(lsg_ctx* ctx, const lsg_grid* g, const double* field, int fixed_dim, int index, double* out) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        // contour.cpp:101-106
+        if (g->dim < 3) fail(LSG_EINVAL, "slice_2d: field must be at least 3-D");
+        if (fixed_dim < 0 || fixed_dim >= g->dim) fail(LSG_EINVAL, "slice_2d: fixed dimension out of range");
+        if (index < 0 || index >= g->counts[fixed_dim]) fail(LSG_EINVAL, "slice_2d: slice index out of range");
+        if (g->dim != 3) fail(LSG_EINVAL, "slice_2d: the device path slices 3-D fields");
+        long long st[LSG_MAX_DIM], acc = 1;
+        for (int d = 0; d < g->dim; ++d) st[d] = acc, acc *= g->counts[d];
+        int kept[2], k = 0;
+        for (int d = 0; d < 3; ++d)
+            if (d != fixed_dim) kept[k++] = d;
+        const long long N = node_count(g);
+        const long long total = static_cast<long long>(g->counts[kept[0]]) * g->counts[kept[1]];
+        double* df = ctx->staging(0, sizeof(double) * N);
+        double* dout = ctx->staging(1, sizeof(double) * total);
+        CUDA_CHECK(cudaMemcpyAsync(df, field, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+        launch_slice(df, total, g->counts[kept[0]], st[kept[0]], st[kept[1]], index * st[fixed_dim], dout, ctx->stream);
+        ctx->note_launch();
+        CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * total, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int lsg_pad_ghost(lsg_ctx* ctx, const lsg_grid* g, const double* field, int dim, int width, double* out) {
     return guarded([&] {
         activate(ctx);

@@ -55,5 +55,11 @@ void launch_shift(const double* padded, double* out, long long N, int n, long lo
 void launch_restrict(const double* in, double* out, long long n, int direction, cudaStream_t st);
 void launch_shape(const ShapeParams& S, cudaStream_t st);
 void launch_range_init(unsigned long long* r, long long nslots, cudaStream_t st);
+long long zero_set_2d(const double* f, int nx, int ny, const double* ax, const double* ay, double dx, double dy,
+                      double* seg_dev, long long cap, int* scratch_counts, int* scratch_offsets, void* temp,
+                      size_t temp_bytes, cudaStream_t st, int* total_host);
+size_t zero_set_temp_bytes(int ncells);
+void launch_slice(const double* f, long long total, int n0, long long s0, long long s1, long long fixed_offset,
+                  double* out, cudaStream_t st);
 
 }  // namespace lsg

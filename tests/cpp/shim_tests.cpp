@@ -287,6 +287,18 @@ static void reachability_tests() {  // test_reachability.cpp:59-285, acceptance.
     CHECK(cfl);
 }
 
+static void contour_tests() {  // contour.cpp via the drop-in
+    const ProblemSetup rot = rigid_rotation_problem(101);
+    const auto segs = extract_zero_set_2d(rot.initial_value);
+    CHECK(!segs.empty());
+    const double len = polyline_length(segs);
+    CHECK(std::abs(len - 2.0 * std::numbers::pi * 0.5) < 0.01);  // circle of radius 0.5
+    const ProblemSetup rk = build_rocket_problem(21);
+    const ScalarField sl = slice_2d(rk.initial_value, 2, 3);
+    CHECK(sl.grid().dim() == 2 && sl.size() == 21u * 21u);
+    CHECK_THROWS_AS(extract_zero_set_2d(rk.initial_value), std::invalid_argument);
+}
+
 int main() {
     try {
         grid_tests();
@@ -294,6 +306,7 @@ int main() {
         hamiltonian_tests();
         integrator_tests();
         reachability_tests();
+        contour_tests();
     } catch (const std::exception& e) {
         std::printf("FAIL uncaught exception: %s\n", e.what());
         return 2;

@@ -412,3 +412,49 @@ def test_step_log_capacity_retry(ctx, port):
     rk, rt, rs = port.solve_brt(S.grid, S.problem, v0, (0.0, 0.2), 3, S.method)
     assert_bitwise(ck, rk, "checkpoints")
     assert_bitwise(steps, rs, "steps")
+
+
+def _ref_zero_set(ref, g, v):
+    import ctypes as C
+
+    cap = 1 << 18
+    seg = np.empty((cap, 4))
+    n, length = C.c_size_t(), C.c_double()
+    assert ref.lib.ref_extract_zero_set_2d(C.byref(g), abi.dptr(np.ascontiguousarray(v)), abi.dptr(seg),
+                                           C.c_size_t(cap), C.byref(n), C.byref(length)) == 0
+    return seg[: n.value], length.value
+
+
+@pytest.mark.parametrize("case", ["circle", "random_saddles", "cfg1_after_solve"])
+def test_zero_set_matches_reference(ctx, port, ref, case):
+    """contour.cpp:27-97 on the device: same segments, same order, same bits."""
+    if case == "circle":
+        S = P.rotation(101)
+        g, v = S.grid, H.initial_value(port, S)
+    elif case == "random_saddles":
+        g = abi.make_grid([-1.0, 0.0], [1.0, 3.0], [37, 29])
+        v = H.random_field(g, 5)  # many saddle cells (codes 5 and 10)
+    else:
+        S = P.cfg1_circle(101)
+        g = S.grid
+        v, _, _ = ctx.integrate(g, S.problem, S.method, 0.0, 0.5, H.initial_value(port, S))
+    seg = ctx.extract_zero_set_2d(g, v)
+    rseg, rlen = _ref_zero_set(ref, g, v)
+    assert len(seg) == len(rseg) > 0
+    assert_bitwise(seg, rseg, "segments")
+    length = float(np.hypot(seg[:, 2] - seg[:, 0], seg[:, 3] - seg[:, 1]).sum())
+    assert abs(length - rlen) <= 1e-12 * rlen
+
+
+def test_slice_2d_matches_reference(ctx, port, ref):
+    import ctypes as C
+
+    S = P.cfg2_air3d(21)
+    v = H.initial_value(port, S)
+    for fixed, idx in [(2, 7), (0, 3), (1, 20)]:
+        out = ctx.slice_2d(S.grid, v, fixed, idx)
+        r = np.empty_like(out)
+        assert ref.lib.ref_slice_2d(C.byref(S.grid), abi.dptr(v), fixed, idx, abi.dptr(r)) == 0
+        assert_bitwise(out, r, f"slice {fixed}={idx}")
+    with pytest.raises(ValueError):
+        ctx.slice_2d(S.grid, v, 2, 21)
