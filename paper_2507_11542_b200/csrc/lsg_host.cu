@@ -237,6 +237,11 @@ bool kernel_choice(const char* name) {
     return e && std::string(e) == name;
 }
 
+bool pdl_enabled() {
+    const char* e = std::getenv("LSG_PDL");
+    return !(e && std::string(e) == "0");
+}
+
 bool force_generic() {
     const char* e = std::getenv("LSG_KERNEL");
     return e && std::string(e) == "generic";
@@ -682,13 +687,30 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
             if (zhi - zlo < M.zchunk) M.zchunk = zhi - zlo;
             const dim3 grid(sl.m3_grid.x, static_cast<unsigned>((zhi - zlo + M.zchunk - 1) / M.zchunk));
             void* args[] = {&P, &M};
-            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), grid,
-                                        dim3(static_cast<unsigned>(s->m3_threads)), args, s->m3_smem, ctx->stream));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(static_cast<unsigned>(s->m3_threads));
+            cfg.dynamicSmemBytes = s->m3_smem;
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL with the previous stage
+            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), args));
         } else {
             void* args[] = {&P};
             const long long n = static_cast<long long>(zhi - zlo) * s->plane;
-            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->fn[mode]), dim3((unsigned)((n + 255) / 256)),
-                                        dim3(256), args, 0, ctx->stream));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)((n + 255) / 256));
+            cfg.blockDim = dim3(256);
+            cfg.stream = ctx->stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->fn[mode]), args));
         }
         ctx->note_launch();
         }

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ Stag
     const long long idx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
     if (idx < (long long)P.zhi * P.plane) {
         int i[D], ix[D];
         double x[D];
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ Stag
         P.out[idx] = o;
         kmin = kmax = order_key(o);
     }
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (P.flags) {
         if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
     }

@@ -234,6 +234,10 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
             }
     };
 
+    // Programmatic dependent launch: everything above is independent of the
+    // previous stage; wait for it before the first read of its output.
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+
     // ---- prologue: u-planes zs-W .. zs+W+D-1 in flight, then the first 2W+1 resident
 #pragma unroll 1
     for (int p = zs - W; p < zs + W + D; ++p) issue(p);
@@ -351,6 +355,7 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
         tr = trn;
     }
     cp_async_wait<0>();
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     if (P.flags && __any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
     if (RANGE && P.range) {
