@@ -26,6 +26,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -74,22 +75,67 @@ int guarded(F&& f) {
     }
 }
 
+// Device buffers come from a per-device stream-ordered pool owned by the
+// library: building and tearing down a solver then costs microseconds instead
+// of the milliseconds cudaMalloc/cudaFree take (tools/alloc_probe.cu).  The
+// pool keeps up to kPoolKeep bytes of freed memory for reuse and returns the
+// rest to the device at the next synchronisation, so it does not hoard memory
+// from other allocators in the process (e.g. torch's).
+constexpr uint64_t kPoolKeep = 1ull << 30;
+
+cudaMemPool_t lib_pool(int device) {
+    static std::mutex m;
+    static cudaMemPool_t pools[256] = {};
+    std::lock_guard<std::mutex> lock(m);
+    if (device < 0 || device >= 256) fail(LSG_EINVAL, "device ordinal out of range");
+    if (!pools[device]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t pool = nullptr;
+        cudaError_t e = cudaMemPoolCreate(&pool, &props);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            fail(LSG_ECUDA, std::string("cudaMemPoolCreate: ") + cudaGetErrorString(e));
+        }
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[device] = pool;
+    }
+    return pools[device];
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t st = nullptr;  // allocation / release stream (the owning context's)
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    void alloc(size_t b) {
-        if (p) cudaFree(p);
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr, o.bytes = 0; }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         bytes = 0;
+    }
+    // Stream-ordered on `stream`; callers synchronise it before handing the
+    // memory to other streams (make_solver does, staging users stay on it).
+    void alloc(size_t b, cudaStream_t stream) {
+        release();
+        st = stream;
         if (b == 0) return;
-        const cudaError_t e = cudaMalloc(&p, b);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool = lib_pool(dev);
+        cudaError_t e = cudaMallocFromPoolAsync(&p, b, pool, stream);
+        if (e == cudaErrorMemoryAllocation) {  // hand retained memory back and retry once
+            cudaGetLastError();
+            cudaStreamSynchronize(stream);
+            cudaMemPoolTrimTo(pool, 0);
+            e = cudaMallocFromPoolAsync(&p, b, pool, stream);
+        }
         if (e != cudaSuccess) {
             p = nullptr;
             cudaGetLastError();
@@ -180,6 +226,8 @@ struct lsg_ctx {
     int nranks = 1;
     ncclComm_t comm = nullptr;
     DevBuf scratch[4];  // stateless-call staging
+    lsg_solver* cached = nullptr;  // last solver built by a stateless call (see cached_solver)
+    std::string cached_key;
 
     void note_launch(int n = 1) {
         launches += static_cast<uint64_t>(n);
@@ -187,7 +235,7 @@ struct lsg_ctx {
         if (e != cudaSuccess) fail(LSG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
     }
     double* staging(int k, size_t bytes) {
-        if (scratch[k].bytes < bytes) scratch[k].alloc(bytes);
+        if (scratch[k].bytes < bytes) scratch[k].alloc(bytes, stream);
         return scratch[k].as<double>();
     }
 };
@@ -333,6 +381,7 @@ struct lsg_solver {
     cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     ~lsg_solver() {
+        if (comm) cudaStreamSynchronize(comm);  // halo traffic done before the buffers go back to the pool
         if (ev_ready) cudaEventDestroy(ev_ready);
         if (ev_halo) cudaEventDestroy(ev_halo);
         if (comm) cudaStreamDestroy(comm);
@@ -481,7 +530,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         }
         const long long padded = static_cast<long long>(sl.nz + 2 * s->halo_w) * s->plane;
         for (int b = 0; b < nbuf; ++b) {
-            sl.buf[b].alloc(sizeof(double) * static_cast<size_t>(padded));
+            sl.buf[b].alloc(sizeof(double) * static_cast<size_t>(padded), ctx->stream);
             sl.f[b] = sl.buf[b].as<double>() + static_cast<long long>(s->halo_w) * s->plane;
         }
         s->slabs.push_back(std::move(sl));
@@ -503,8 +552,9 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         s_off[d] = host.size();
         for (int i = 0; i < g->counts[d]; ++i) host.push_back(std::sin(host[ax_off[d] + i]));
     }
-    s->tables.alloc(sizeof(double) * host.size());
-    CUDA_CHECK(cudaMemcpy(s->tables.p, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice));
+    s->tables.alloc(sizeof(double) * host.size(), ctx->stream);
+    CUDA_CHECK(cudaMemcpyAsync(s->tables.p, host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
     const double* base = s->tables.as<double>();
     for (int d = 0; d < s->D; ++d) {
         s->axis[d] = base + ax_off[d];
@@ -514,18 +564,67 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         }
         s->lc[d] = line_const(g, d);
     }
-    s->dflags.alloc(sizeof(unsigned) * 2);
-    s->dalpha.alloc(sizeof(unsigned long long) * 8);
+    s->dflags.alloc(sizeof(unsigned) * 2, ctx->stream);
+    s->dalpha.alloc(sizeof(unsigned long long) * 8, ctx->stream);
     CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, s->dflags.bytes, ctx->stream));
-    s->drange.alloc(sizeof(unsigned long long) * 2 * kRingSlots);
+    s->drange.alloc(sizeof(unsigned long long) * 2 * kRingSlots, ctx->stream);
     s->range_cap = kRingSlots;
     CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, s->drange.bytes, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // buffers usable from any stream from here on
     return s;
+}
+
+// The stateless reference-facing calls (term_lax_friedrichs, integrate,
+// solve_brt) rebuild nothing when called again on the same grid, problem and
+// integrator: the context keeps the last solver (device fields, axis/trig
+// tables, alpha) keyed on the descriptors' bytes and the kernel-selection
+// environment.  LSG_CALL_CACHE=0 disables it.
+std::string solver_key(const lsg_grid* g, const lsg_problem* p, int method) {
+    std::string k;
+    auto put = [&k](const void* x, size_t n) { k.append(static_cast<const char*>(x), n); };
+    put(&g->dim, sizeof g->dim);
+    const int D = std::max(0, std::min(g->dim, kMaxDim));
+    put(g->counts, sizeof(int) * D);
+    put(g->mins, sizeof(double) * D);
+    put(g->maxs, sizeof(double) * D);
+    put(&g->periodic_mask, sizeof g->periodic_mask);
+    put(&p->kind, sizeof p->kind);
+    put(&p->scheme, sizeof p->scheme);
+    put(&p->direction, sizeof p->direction);
+    put(&p->restrict_update, sizeof p->restrict_update);
+    put(&p->options, sizeof p->options);
+    put(p->params, sizeof p->params);
+    put(&method, sizeof method);
+    for (const char* e : {"LSG_KERNEL", "LSG_M3_R", "LSG_M3_CHUNK"}) {
+        const char* v = std::getenv(e);
+        k += '|';
+        if (v) k += v;
+    }
+    return k;
+}
+
+lsg_solver* cached_solver(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int method) {
+    activate(ctx);
+    check_grid(g);
+    if (!p) fail(LSG_EINVAL, "term_lax_friedrichs: problem must provide ham_func and dissipation_bounds");
+    const char* off = std::getenv("LSG_CALL_CACHE");
+    const bool enabled = !(off && std::string(off) == "0");
+    std::string key = solver_key(g, p, method);
+    if (enabled && ctx->cached && ctx->cached_key == key) {
+        ctx->cached->cur = 0;
+        return ctx->cached;
+    }
+    delete ctx->cached;  // release its device memory before allocating the next
+    ctx->cached = nullptr;
+    ctx->cached_key.clear();
+    ctx->cached = make_solver(ctx, g, p, method, 1).release();
+    ctx->cached_key = enabled ? std::move(key) : std::string("\x01disabled");
+    return ctx->cached;
 }
 
 void ensure_range(lsg_solver* s, long long nslots) {
     if (s->range_cap < nslots) {
-        s->drange.alloc(sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots));
+        s->drange.alloc(sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots), s->ctx->stream);
         s->range_cap = nslots;
     }
     CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots),
@@ -982,8 +1081,9 @@ int lsg_ctx_destroy(lsg_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        delete ctx->cached;
         if (ctx->comm) ncclCommDestroy(ctx->comm);
-        for (auto& b : ctx->scratch) b.alloc(0);
+        for (auto& b : ctx->scratch) b.release();
         cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -1272,20 +1372,20 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
                 double* step_bound) {
     (void)t;
     return guarded([&] {
-        auto s = make_solver(ctx, g, p, LSG_CFL1, 1);
+        lsg_solver* s = cached_solver(ctx, g, p, LSG_CFL1);
         if (!s->invalid.empty()) fail(LSG_EINVAL, s->invalid);
-        upload(s.get(), v, 0);
-        ensure_alpha(s.get());
+        upload(s, v, 0);
+        ensure_alpha(s);
         CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
-        launch_stage(s.get(), MODE_TERM, 0, -1, 1, 0.0, 0.0, nullptr);
+        launch_stage(s, MODE_TERM, 0, -1, 1, 0.0, 0.0, nullptr);
         unsigned flags = 0;
         CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof flags, cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
         // hamiltonian.cpp:37-56: H is validated before the bounds
         if (flags & FLAG_HAM_NONFINITE)
             fail(LSG_ENUMERIC, "term_lax_friedrichs: hamiltonian produced a non-finite value");
-        check_alpha_valid(s.get());
-        download(s.get(), dvdt, 1);
+        check_alpha_valid(s);
+        download(s, dvdt, 1);
         *step_bound = s->bound;
     });
 }
@@ -1308,12 +1408,12 @@ int lsg_integrate(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int met
                   const lsg_opts* opts, lsg_steplog* steps, size_t log_cap, size_t* n_steps, double* t_final) {
     return guarded([&] {
         if (opts) check_options(opts);
-        auto s = make_solver(ctx, g, p, method, 1);
-        LegPlan plan = plan_leg(s.get(), t0, tf, opts);
+        lsg_solver* s = cached_solver(ctx, g, p, method);
+        LegPlan plan = plan_leg(s, t0, tf, opts);
         check_log_room(plan.log.size(), steps, log_cap, n_steps);
-        upload(s.get(), v, 0);
-        run_leg(s.get(), plan);
-        download(s.get(), v, s->cur);
+        upload(s, v, 0);
+        run_leg(s, plan);
+        download(s, v, s->cur);
         copy_log(plan.log, steps, log_cap, n_steps);
         if (t_final) *t_final = plan.t_final;
     });
@@ -1337,7 +1437,7 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
         if (n_steps) *n_steps = 0;
         if (integration_seconds) *integration_seconds = 0.0;
         if (duration == 0.0 || n_checkpoints == 1) return;
-        auto s = make_solver(ctx, g, p, method, 1);
+        lsg_solver* s = cached_solver(ctx, g, p, method);
         const int segments = n_checkpoints - 1;
         // every leg's schedule up front (reachability.cpp:160-170: the next leg
         // starts from leg.t), so the log capacity is known before device work
@@ -1346,20 +1446,20 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
         double t = 0.0;
         for (int k = 1; k <= segments; ++k) {
             const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
-            plans.push_back(plan_leg(s.get(), t, t_end, opts));
+            plans.push_back(plan_leg(s, t, t_end, opts));
             t = plans.back().t_final;
             total += plans.back().log.size();
             if (plans.back().collapsed) break;
         }
         check_log_room(total, steps, log_cap, n_steps);
-        upload(s.get(), v0, 0);
+        upload(s, v0, 0);
         std::vector<lsg_steplog> all;
         const auto start = std::chrono::steady_clock::now();
         for (int k = 1; k <= static_cast<int>(plans.size()); ++k) {
             const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
-            run_leg(s.get(), plans[k - 1]);
+            run_leg(s, plans[k - 1]);
             all.insert(all.end(), plans[k - 1].log.begin(), plans[k - 1].log.end());
-            download(s.get(), checkpoints + static_cast<long long>(k) * N, s->cur);
+            download(s, checkpoints + static_cast<long long>(k) * N, s->cur);
             checkpoint_times[k] = t_end;
             *n_out = k + 1;
         }
@@ -1390,7 +1490,9 @@ int lsg_solver_destroy(lsg_solver* s) {
     return guarded([&] {
         if (!s) return;
         cudaSetDevice(s->ctx->device);
-        cudaStreamSynchronize(s->ctx->stream);
+        // work a caller queued on lsg_solver_field_device's pointer from its own
+        // streams must finish before the memory is recycled
+        cudaDeviceSynchronize();
         delete s;
     });
 }
