@@ -17,3 +17,21 @@ def test_cpp_dropin_reference_cases():
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failures" in out.stdout
+
+
+def test_cpp_dropin_reference_benchmark_outputs():
+    """The reference's own microbenchmark suite (benchmarks/bench_kernels.cpp,
+    from proj/benchmarks/bench_kernels.cpp) built against the drop-in: every
+    case's output checksum equals the reference build's bit for bit
+    (tests/golden/bench_kernels_checksums.json)."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    binary = os.path.join(root, "benchmarks", "bench_kernels_b200")
+    assert os.path.exists(binary), "benchmarks/bench_kernels_b200 not built: run __graft_entry__.build()"
+    out = subprocess.run([binary, "--large", "--min-time", "0"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    got = {r["name"]: r["checksum"] for r in map(json.loads, filter(None, out.stdout.splitlines()))}
+    want = json.load(open(os.path.join(root, "tests", "golden", "bench_kernels_checksums.json")))["checksums"]
+    assert set(got) == set(want)
+    bad = {k: (got[k], want[k]) for k in want if got[k] != want[k]}
+    assert not bad, bad
