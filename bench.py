@@ -219,9 +219,11 @@ def b200_arm(args):
 
     ws, rank, local = dist_env()
     dist = None
-    if ws > 1:
+    if ws > 1 or args.dist_selftest:
         import torch.distributed as dist
 
+        if ws == 1:  # one-rank NCCL communicator through the multi-rank branch
+            os.environ["LSG_DIST_SELFTEST"] = "1"
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -355,7 +357,7 @@ def b200_arm(args):
             "grid": [setup.grid.counts[d] for d in range(setup.grid.dim)],
             "nodes_per_gpu": nodes_local,
             "scheme": "ENO3", "integrator": "odeCFL3 (TVD-RK3)", "clamp": "Grow",
-            "parallelism": f"slab{ws}" if ws > 1 else "single",
+            "parallelism": f"slab{ws}" if ws > 1 else ("slab1 (NCCL self-test)" if args.dist_selftest else "single"),
             "l2": "flushed before every timed step (512 MiB write); inputs 8.2 MB/field fit in L2",
             "timing": "one CUDA event pair on the launching stream around each step (after its L2 flush), "
                       "summed; max over ranks; per-stage times from 20 extra untimed steps",
@@ -414,6 +416,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="under torchrun with one rank: run the multi-rank (NCCL) branch on a one-rank communicator")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

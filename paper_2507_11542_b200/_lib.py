@@ -83,7 +83,7 @@ class Context:
 
     def __init__(self, device=0, rank=0, nranks=1, nccl_id=None):
         h = C.c_void_p()
-        if nranks > 1:
+        if nranks > 1 or nccl_id is not None:
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("distributed context needs the 128-byte NCCL unique id")
             buf = (C.c_ubyte * 128).from_buffer_copy(bytes(nccl_id))

@@ -18,7 +18,8 @@ __global__ void __launch_bounds__(256) box3_kernel(const __grid_constant__ Stage
     const int n0 = P.n[0], n1 = P.n[1];
     const int plane = n0 * n1;
     const int q = blockIdx.x * 256 + threadIdx.x;
-    const int z = P.zlo + blockIdx.y;
+    const int zl = P.zlo + blockIdx.y;
+    const int z = zl >= P.zsplit ? zl + P.zskip : zl;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
     if (q < plane) {

@@ -224,6 +224,7 @@ struct lsg_ctx {
     uint64_t launches = 0;
     int rank = 0;
     int nranks = 1;
+    bool dist_selftest = false;  // one-rank communicator driving the distributed branch (LSG_DIST_SELFTEST)
     ncclComm_t comm = nullptr;
     DevBuf scratch[4];  // stateless-call staging
     lsg_solver* cached = nullptr;  // last solver built by a stateless call (see cached_solver)
@@ -378,12 +379,19 @@ struct lsg_solver {
     size_t m3_smem = 0;
     std::string invalid;  // deferred invalid_argument (raised at the first term evaluation)
     int cur = 0;
+    // halo planes of buffer b hold the neighbours' current boundary planes
+    // (set by the exchange that follows each stage's boundary bands; cleared
+    // whenever the field is written from outside a stage)
+    bool halo_ok[3] = {false, false, false};
     cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
-    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    cudaStream_t side = nullptr;  // boundary bands, concurrent with the interior (slabs only)
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr, ev_main = nullptr, ev_bnd = nullptr;
     ~lsg_solver() {
         if (comm) cudaStreamSynchronize(comm);  // halo traffic done before the buffers go back to the pool
-        if (ev_ready) cudaEventDestroy(ev_ready);
-        if (ev_halo) cudaEventDestroy(ev_halo);
+        if (side) cudaStreamSynchronize(side);
+        for (cudaEvent_t e : {ev_ready, ev_halo, ev_main, ev_bnd})
+            if (e) cudaEventDestroy(e);
+        if (side) cudaStreamDestroy(side);
         if (comm) cudaStreamDestroy(comm);
     }
 };
@@ -411,15 +419,22 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->method = method;
     s->D = g->dim;
     s->W = ghost_width(p->scheme);
-    s->distributed = ctx->nranks > 1;
+    s->distributed = ctx->nranks > 1 || ctx->dist_selftest;
     s->P = s->distributed ? ctx->nranks : nslabs;
     s->total = node_count(g);
     for (int d = 0; d + 1 < s->D; ++d) s->plane *= g->counts[d];
-    s->halo_w = s->P > 1 ? s->W : 0;
+    s->halo_w = (s->P > 1 || s->distributed) ? s->W : 0;
     if (s->halo_w) {
-        CUDA_CHECK(cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking));
+        // halo traffic and boundary bands sit on the critical path of the next
+        // stage: their blocks go ahead of the interior's when SMs free up
+        int lo_prio = 0, hi_prio = 0;
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&s->comm, cudaStreamNonBlocking, hi_prio));
         CUDA_CHECK(cudaEventCreateWithFlags(&s->ev_ready, cudaEventDisableTiming));
         CUDA_CHECK(cudaEventCreateWithFlags(&s->ev_halo, cudaEventDisableTiming));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, hi_prio));
+        CUDA_CHECK(cudaEventCreateWithFlags(&s->ev_main, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&s->ev_bnd, cudaEventDisableTiming));
     }
     const int nlast = g->counts[s->D - 1];
     if (s->P > nlast) fail(LSG_EINVAL, "slab decomposition: more slabs than planes along the last axis");
@@ -722,32 +737,27 @@ void exchange(lsg_solver* s, int b, cudaStream_t st) {
 // zlo/zhi: plane range [zlo, zhi) of every slab (zhi < 0: up to the slab end,
 // measured from the end when zlo < 0 is not used).
 void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range,
-                  int part = 0) {
+                  int part, cudaStream_t stream) {
     lsg_ctx* ctx = s->ctx;
     const int D = s->D;
     for (Slab& sl : s->slabs) {
         // part 0: all planes; 1: interior planes [W, nz-W) that need no ghost
-        // planes; 2: the two boundary bands (launched after the exchange)
-        int zlo = 0, zhi = sl.nz;
+        // planes; 2: both boundary bands [0, W) and [nz-W, nz) in one launch
+        // (logical planes [0, 2W) with a gap of nz-2W planes after W)
+        int zlo = 0, zhi = sl.nz, zsplit = 0, zskip = 0;
         const int W = s->halo_w;
         if (part == 1) {
             zlo = W, zhi = sl.nz - W;
             if (zhi <= zlo) continue;
+        } else if (part == 2 && sl.nz > 2 * W) {
+            zhi = 2 * W, zsplit = W, zskip = sl.nz - 2 * W;
         }
-        for (int band = 0; band < (part == 2 ? 2 : 1); ++band) {
-        if (part == 2) {
-            if (sl.nz <= 2 * W) {
-                if (band == 1) break;
-                zlo = 0, zhi = sl.nz;
-            } else if (band == 0) {
-                zlo = 0, zhi = W;
-            } else {
-                zlo = sl.nz - W, zhi = sl.nz;
-            }
-        }
+        {
         StageParams P{};
         P.zlo = zlo;
         P.zhi = zhi;
+        P.zsplit = zsplit;
+        P.zskip = zskip;
         P.plane = s->plane;
         P.u = sl.f[ui];
         P.v0 = vi >= 0 ? sl.f[vi] : nullptr;
@@ -780,17 +790,18 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
             const long long pl = s->plane;
             CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->b3fn[mode][range ? 1 : 0]),
                                         dim3(static_cast<unsigned>((pl + 255) / 256), static_cast<unsigned>(zhi - zlo)),
-                                        dim3(256), args, 0, ctx->stream));
+                                        dim3(256), args, 0, stream));
         } else if (s->m3fn[mode][0]) {
             March3 M = sl.m3;
             if (zhi - zlo < M.zchunk) M.zchunk = zhi - zlo;
+            if (zskip) M.zchunk = W;  // one chunk per band: none straddles the gap
             const dim3 grid(sl.m3_grid.x, static_cast<unsigned>((zhi - zlo + M.zchunk - 1) / M.zchunk));
             void* args[] = {&P, &M};
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = grid;
             cfg.blockDim = dim3(static_cast<unsigned>(s->m3_threads));
             cfg.dynamicSmemBytes = s->m3_smem;
-            cfg.stream = ctx->stream;
+            cfg.stream = stream;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL with the previous stage
             attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
@@ -803,7 +814,7 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)((n + 255) / 256));
             cfg.blockDim = dim3(256);
-            cfg.stream = ctx->stream;
+            cfg.stream = stream;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
@@ -816,22 +827,45 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
     }
 }
 
-// One fused stage.  With ghost planes (several slabs) the exchange runs on the
-// communication stream while the interior planes are computed; the boundary
-// bands follow once the halos have arrived.
+// One fused stage over every slab.  Without halos: one launch.  With halos
+// (several slabs or ranks):
+//   side stream: the boundary bands (one launch), once the main stream's
+//                previous stage and the exchange of u's halo are done;
+//   comm stream: the exchange of the bands' fresh output planes (the next
+//                stage's halo), as soon as the bands finish;
+//   main stream: the interior planes, concurrently, then a join on the bands.
+// So the halo traffic overlaps the interior and the next stage finds it done.
+// A field written from outside a stage (upload, device copy, initial shape)
+// has no valid halo and is exchanged before its first stage.
 void run_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range) {
+    lsg_ctx* ctx = s->ctx;
     if (s->halo_w == 0) {
-        launch_stage(s, mode, ui, vi, oi, dt, c, range, 0);
+        launch_stage(s, mode, ui, vi, oi, dt, c, range, 0, ctx->stream);
         return;
     }
-    lsg_ctx* ctx = s->ctx;
-    CUDA_CHECK(cudaEventRecord(s->ev_ready, ctx->stream));
-    CUDA_CHECK(cudaStreamWaitEvent(s->comm, s->ev_ready, 0));
-    exchange(s, ui, s->comm);
-    CUDA_CHECK(cudaEventRecord(s->ev_halo, s->comm));
-    launch_stage(s, mode, ui, vi, oi, dt, c, range, 1);
-    CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->ev_halo, 0));
-    launch_stage(s, mode, ui, vi, oi, dt, c, range, 2);
+    auto exchange_after = [&](cudaEvent_t ev, cudaStream_t from, int b) {
+        CUDA_CHECK(cudaEventRecord(ev, from));
+        CUDA_CHECK(cudaStreamWaitEvent(s->comm, ev, 0));
+        exchange(s, b, s->comm);
+        CUDA_CHECK(cudaEventRecord(s->ev_halo, s->comm));
+    };
+    if (!s->halo_ok[ui]) {
+        exchange_after(s->ev_ready, ctx->stream, ui);
+        s->halo_ok[ui] = true;
+    }
+    CUDA_CHECK(cudaEventRecord(s->ev_main, ctx->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(s->side, s->ev_main, 0));
+    CUDA_CHECK(cudaStreamWaitEvent(s->side, s->ev_halo, 0));
+    launch_stage(s, mode, ui, vi, oi, dt, c, range, 2, s->side);
+    if (mode != MODE_TERM && oi != ui) {
+        exchange_after(s->ev_bnd, s->side, oi);  // the next stage's halo
+        s->halo_ok[oi] = true;
+    } else {
+        CUDA_CHECK(cudaEventRecord(s->ev_bnd, s->side));
+        s->halo_ok[oi] = false;
+    }
+    launch_stage(s, mode, ui, vi, oi, dt, c, range, 1, ctx->stream);
+    CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->ev_bnd, 0));
 }
 
 // One TVD-RK step (integrator.cpp:58-85); buffers: cur = v, the others scratch.
@@ -982,8 +1016,13 @@ void copy_log(const std::vector<lsg_steplog>& log, lsg_steplog* out, size_t cap,
         for (size_t k = 0; k < log.size() && k < cap; ++k) out[k] = log[k];
 }
 
+void invalidate_halos(lsg_solver* s) {
+    for (bool& h : s->halo_ok) h = false;
+}
+
 void upload(lsg_solver* s, const double* host, int b) {
     lsg_ctx* ctx = s->ctx;
+    invalidate_halos(s);
     if (s->distributed) {
         const Slab& sl = s->slabs[0];
         CUDA_CHECK(cudaMemcpyAsync(sl.f[b], host, sizeof(double) * sl.nodes, cudaMemcpyHostToDevice, ctx->stream));
@@ -1067,7 +1106,13 @@ int lsg_ctx_create_dist(int device, int rank, int nranks, const void* nccl_id128
         std::unique_ptr<lsg_ctx> owner(c);
         c->rank = rank;
         c->nranks = nranks;
-        if (nranks > 1) {
+        // LSG_DIST_SELFTEST=1 with nranks == 1: a real one-rank NCCL
+        // communicator, and solvers take the distributed branch (halo planes,
+        // NCCL self send/recv on a periodic slab axis, NCCL all-reduces), so
+        // that branch runs on a one-GPU box without ranks waiting on each other.
+        const char* st = std::getenv("LSG_DIST_SELFTEST");
+        c->dist_selftest = nranks == 1 && st && std::string(st) == "1";
+        if (nranks > 1 || c->dist_selftest) {
             ncclUniqueId id;
             std::memcpy(&id, nccl_id128, sizeof id);
             NCCL_CHECK(ncclCommInitRank(&c->comm, nranks, id, rank));
@@ -1377,7 +1422,7 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
         upload(s, v, 0);
         ensure_alpha(s);
         CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
-        launch_stage(s, MODE_TERM, 0, -1, 1, 0.0, 0.0, nullptr);
+        run_stage(s, MODE_TERM, 0, -1, 1, 0.0, 0.0, nullptr);  // halo exchange first on a multi-rank context
         unsigned flags = 0;
         CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof flags, cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -1532,6 +1577,7 @@ int lsg_solver_set_field_device(lsg_solver* s, const double* dev_v) {
     return guarded([&] {
         activate(s->ctx);
         s->cur = 0;
+        invalidate_halos(s);
         for (const Slab& sl : s->slabs) {
             const long long off = s->distributed ? 0 : static_cast<long long>(sl.z0) * s->plane;
             CUDA_CHECK(cudaMemcpyAsync(sl.f[0], dev_v + off, sizeof(double) * sl.nodes, cudaMemcpyDeviceToDevice,
@@ -1544,6 +1590,7 @@ int lsg_solver_field_device(lsg_solver* s, double** dev_v) {
     return guarded([&] {
         if (s->slabs.size() != 1) fail(LSG_EINVAL, "field_device: solver holds several slabs");
         *dev_v = s->slabs[0].f[s->cur];
+        invalidate_halos(s);  // the caller may write through the pointer
     });
 }
 
@@ -1560,6 +1607,7 @@ int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const
                 fail(LSG_EINVAL, "cylinder: at least one dimension must remain active");
         }
         s->cur = 0;
+        invalidate_halos(s);
         for (Slab& sl : s->slabs) {
             ShapeParams S{};
             S.n_local = sl.nodes;

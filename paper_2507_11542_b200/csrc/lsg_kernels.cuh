@@ -25,11 +25,12 @@ using StageFn = void (*)(StageParams);
 template <int D, int S, int KIND, int MODE>
 __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ StageParams P) {
     constexpr int W = SchemeWidth<S>::W;
-    const long long idx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long lidx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long idx = lidx >= (long long)P.zsplit * P.plane ? lidx + (long long)P.zskip * P.plane : lidx;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
-    if (idx < (long long)P.zhi * P.plane) {
+    if (lidx < (long long)P.zhi * P.plane) {
         int i[D], ix[D];
         double x[D];
         long long r = idx;

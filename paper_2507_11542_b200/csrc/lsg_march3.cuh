@@ -108,8 +108,12 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
     const int cols = min(TX, n0 - x0), rows = min(M.R, n1 - y0);
-    const int zs = P.zlo + blockIdx.y * M.zchunk;
-    const int ze = min(zs + M.zchunk, P.zhi);
+    // logical chunk [zsl, zel); a chunk never straddles zsplit (the host
+    // sizes chunks so), so it maps to physical planes as one block
+    const int zsl = P.zlo + blockIdx.y * M.zchunk;
+    const int zel = min(zsl + M.zchunk, P.zhi);
+    const int zs = zsl >= P.zsplit ? zsl + P.zskip : zsl;
+    const int ze = zsl >= P.zsplit ? zel + P.zskip : min(zel, P.zsplit);
     const int yl = t / TX2, pl = t - (t / TX2) * TX2;
     const int xl = 2 * pl;
     const bool active = yl < rows && xl < cols;
