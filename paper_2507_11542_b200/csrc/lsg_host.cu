@@ -525,23 +525,25 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             const int nt = ntx * nty;
             double best = 1e300;
             int best_nzc = 1;
-            for (int nzc = 1; nzc <= sl.nz; ++nzc) {
+            for (int nzc = 1; nzc <= sl.nz; ++nzc) {  // balanced split: chunks of ceil / floor(nz / nzc)
                 const int chunk = (sl.nz + nzc - 1) / nzc;
-                const int used = (sl.nz + chunk - 1) / chunk;
-                const double waves = std::ceil(static_cast<double>(nt) * used / (148.0 * s->m3_per_sm));
+                const double waves = std::ceil(static_cast<double>(nt) * nzc / (148.0 * s->m3_per_sm));
                 const double cost = waves * (chunk + 0.5 * s->W + 1.0);
-                if (cost < best - 1e-9) {
+                if (cost < best + 1e-9) {  // ties: more, shorter chunks balance the SMs better
                     best = cost;
-                    best_nzc = used;
+                    best_nzc = nzc;
                 }
             }
-            int chunk = (sl.nz + best_nzc - 1) / best_nzc;
-            if (const char* e = std::getenv("LSG_M3_CHUNK")) chunk = std::max(1, std::min(sl.nz, std::atoi(e)));
+            int nzc = best_nzc;
+            if (const char* e = std::getenv("LSG_M3_CHUNK")) {  // planes per chunk (tuning override)
+                const int chunk = std::max(1, std::min(sl.nz, std::atoi(e)));
+                nzc = (sl.nz + chunk - 1) / chunk;
+            }
             if (std::getenv("LSG_M3_VERBOSE"))
-                std::fprintf(stderr, "march3: TX=%d R=%d tiles=%d chunk=%d blocks/SM=%d smem=%zu threads=%d\n", TX, R,
-                             nt, chunk, s->m3_per_sm, s->m3_smem, s->m3_threads);
-            sl.m3 = March3{TX, R, ntx, chunk, s->m3_pitch};
-            sl.m3_grid = dim3(static_cast<unsigned>(nt), static_cast<unsigned>((sl.nz + chunk - 1) / chunk));
+                std::fprintf(stderr, "march3: TX=%d R=%d tiles=%d chunks=%d blocks/SM=%d smem=%zu threads=%d\n", TX, R,
+                             nt, nzc, s->m3_per_sm, s->m3_smem, s->m3_threads);
+            sl.m3 = March3{TX, R, ntx, nzc, s->m3_pitch};
+            sl.m3_grid = dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nzc));
         }
         const long long padded = static_cast<long long>(sl.nz + 2 * s->halo_w) * s->plane;
         for (int b = 0; b < nbuf; ++b) {
@@ -793,9 +795,9 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
                                         dim3(256), args, 0, stream));
         } else if (s->m3fn[mode][0]) {
             March3 M = sl.m3;
-            if (zhi - zlo < M.zchunk) M.zchunk = zhi - zlo;
-            if (zskip) M.zchunk = W;  // one chunk per band: none straddles the gap
-            const dim3 grid(sl.m3_grid.x, static_cast<unsigned>((zhi - zlo + M.zchunk - 1) / M.zchunk));
+            if (zhi - zlo < M.nzc) M.nzc = zhi - zlo;
+            if (zskip) M.nzc = 2;  // one chunk per band: none straddles the gap
+            const dim3 grid(sl.m3_grid.x, static_cast<unsigned>(M.nzc));
             void* args[] = {&P, &M};
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = grid;

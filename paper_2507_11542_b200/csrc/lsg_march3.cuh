@@ -25,7 +25,7 @@ struct March3 {
     int TX;      // tile width along x (even)
     int R;       // tile height along y
     int ntx;     // tiles along x
-    int zchunk;  // planes per block
+    int nzc;     // z-chunks per launch: a balanced split, the first (planes % nzc) one plane longer
     int pitch;   // shared-memory row pitch in doubles (even)
 };
 
@@ -108,10 +108,14 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
     const int cols = min(TX, n0 - x0), rows = min(M.R, n1 - y0);
-    // logical chunk [zsl, zel); a chunk never straddles zsplit (the host
-    // sizes chunks so), so it maps to physical planes as one block
-    const int zsl = P.zlo + blockIdx.y * M.zchunk;
-    const int zel = min(zsl + M.zchunk, P.zhi);
+    // logical chunk [zsl, zel) of a balanced split of [zlo, zhi): the longer
+    // chunks come first in launch order, so they spread over distinct SMs in
+    // the first wave.  A chunk never straddles zsplit (the host splits so),
+    // so it maps to physical planes as one block.
+    const int nplanes = P.zhi - P.zlo, cb = nplanes / M.nzc, crem = nplanes - cb * M.nzc;
+    const int cidx = blockIdx.y;
+    const int zsl = P.zlo + cidx * cb + min(cidx, crem);
+    const int zel = zsl + cb + (cidx < crem ? 1 : 0);
     const int zs = zsl >= P.zsplit ? zsl + P.zskip : zsl;
     const int ze = zsl >= P.zsplit ? zel + P.zskip : min(zel, P.zsplit);
     const int yl = t / TX2, pl = t - (t / TX2) * TX2;
@@ -177,14 +181,25 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     }
 
     const int nglob = P.nz_glob;
-    auto uslot = [&](int p) { return ring + ((p - zs + W) % NB) * plane_sz; };
-    auto vslot = [&](int p) { return vring + ((p - zs) % NV) * vplane_sz; };
+    // Ring slots: u-plane p lives in slot (p - zs + W) mod NB, v0-plane p in
+    // (p - zs) mod NV.  Planes are issued, ghost-filled and consumed strictly in
+    // order, so each of those walks keeps its own running offset (no modulo).
+    const int ring_sz = NB * plane_sz, vring_sz = NV * vplane_sz;
+    int is_off = 0, vi_off = 0;  // next u / v0 plane to issue
+    int gp_off = 0;              // next u plane to ghost-fill
+    auto bump = [](int& off, int step, int size) {
+        off += step;
+        if (off == size) off = 0;
+    };
+    bool has_ghost = false;
+#pragma unroll
+    for (int q = 0; q < kMaxHalo; ++q) has_ghost |= hdst[q] >= 0 && hsrc[q] < 0;
 
     // Issue the async copies of u-plane p (chunk-relative window [zs-W, ze+W))
     // and of v0-plane p-W, as one commit group.
     auto issue = [&](int p) {
         if (p < ze + W) {
-            double* buf = uslot(p);
+            double* buf = ring + is_off;
             const int zg = P.z0 + p;
             int src = p;
             bool ghost_plane = false;
@@ -219,23 +234,27 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
         if (MODE == MODE_COMBINE) {
             const int pv = p - W;
             if (pv >= zs && pv < ze) {
-                double* vb = vslot(pv);
+                double* vb = vring + vi_off;
+                bump(vi_off, vplane_sz, vring_sz);
                 const double* base = P.v0 + (long long)pv * s2;
                 if (active) cp_async8(vb + vme, base + coli);
                 if (two) cp_async8(vb + vme + 1, base + coli + 1);
             }
         }
         cp_async_commit();
+        bump(is_off, plane_sz, ring_sz);
     };
     auto ghost_pass = [&](int p) {
-        if (p >= ze + W) return;
-        double* buf = uslot(p);
+        if (has_ghost && p < ze + W) {
+            double* buf = ring + gp_off;
 #pragma unroll
-        for (int q = 0; q < kMaxHalo; ++q)
-            if (hdst[q] >= 0 && hsrc[q] < 0) {
-                const double a = buf[ga[q]];
-                buf[hdst[q]] = a + gk[q] * (a - buf[gb[q]]);
-            }
+            for (int q = 0; q < kMaxHalo; ++q)
+                if (hdst[q] >= 0 && hsrc[q] < 0) {
+                    const double a = buf[ga[q]];
+                    buf[hdst[q]] = a + gk[q] * (a - buf[gb[q]]);
+                }
+        }
+        bump(gp_off, plane_sz, ring_sz);
     };
 
     // Programmatic dependent launch: everything above is independent of the
@@ -257,21 +276,22 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     double az = __ldg(P.axis[2] + P.z0 + zs);
     Trig tr = load_trig<KIND>(P, P.z0 + zs, 0);
 
-    int j0 = 0;  // ring slot of plane z-W (advances by one per plane)
+    // ring offsets (own pair slot included) of the 2W+1 resident planes
+    // z-W..z+W, shifted by one plane per iteration
+    int zoff[2 * W + 1];
+#pragma unroll
+    for (int k = 0; k < 2 * W + 1; ++k) zoff[k] = k * plane_sz + me;
+    int znext = (2 * W + 1) * plane_sz;  // slot of plane z+W+1 (NB > 2W+1)
+    int vr_off = 0;                      // v0 ring slot of plane z
 #pragma unroll 1
     for (int z = zs; z < ze; ++z) {
         cp_async_wait<D - 1>();  // u-plane z+W (and v0-plane z) complete for this thread
         __syncthreads();         // ... and for every thread; slot of z-W-1 is free
         ghost_pass(z + W);
         issue(z + W + D);
-        // the 2W+1 resident planes z-W..z+W sit in ring slots j0, j0+1, ... (mod NB)
         const double* zpl[2 * W + 1];
 #pragma unroll
-        for (int k = 0; k < 2 * W + 1; ++k) {
-            const int j = j0 + k;
-            zpl[k] = ring + (j >= NB ? j - NB : j) * plane_sz + me;
-        }
-        j0 = j0 + 1 == NB ? 0 : j0 + 1;
+        for (int k = 0; k < 2 * W + 1; ++k) zpl[k] = ring + zoff[k];
         double azn = 0.0;
         Trig trn;
         if (z + 1 < ze) {
@@ -335,7 +355,7 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
             }
             double b0 = 0.0, b1 = 0.0;
             if (MODE == MODE_COMBINE) {
-                const double2 v = *reinterpret_cast<const double2*>(vslot(z) + vme);
+                const double2 v = *reinterpret_cast<const double2*>(vring + vr_off + vme);
                 b0 = v.x;
                 b1 = v.y;
             }
@@ -357,6 +377,11 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
         }
         az = azn;
         tr = trn;
+#pragma unroll
+        for (int k = 0; k < 2 * W; ++k) zoff[k] = zoff[k + 1];
+        zoff[2 * W] = znext + me;
+        bump(znext, plane_sz, ring_sz);
+        bump(vr_off, vplane_sz, vring_sz);
     }
     cp_async_wait<0>();
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
