@@ -276,22 +276,22 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     double az = __ldg(P.axis[2] + P.z0 + zs);
     Trig tr = load_trig<KIND>(P, P.z0 + zs, 0);
 
-    // ring offsets (own pair slot included) of the 2W+1 resident planes
-    // z-W..z+W, shifted by one plane per iteration
-    int zoff[2 * W + 1];
-#pragma unroll
-    for (int k = 0; k < 2 * W + 1; ++k) zoff[k] = k * plane_sz + me;
-    int znext = (2 * W + 1) * plane_sz;  // slot of plane z+W+1 (NB > 2W+1)
-    int vr_off = 0;                      // v0 ring slot of plane z
+    int j0 = 0;      // ring slot of plane z-W (advances by one per plane)
+    int vr_off = 0;  // v0 ring offset of plane z
 #pragma unroll 1
     for (int z = zs; z < ze; ++z) {
         cp_async_wait<D - 1>();  // u-plane z+W (and v0-plane z) complete for this thread
         __syncthreads();         // ... and for every thread; slot of z-W-1 is free
         ghost_pass(z + W);
         issue(z + W + D);
+        // the 2W+1 resident planes z-W..z+W sit in ring slots j0, j0+1, ... (mod NB)
         const double* zpl[2 * W + 1];
 #pragma unroll
-        for (int k = 0; k < 2 * W + 1; ++k) zpl[k] = ring + zoff[k];
+        for (int k = 0; k < 2 * W + 1; ++k) {
+            const int j = j0 + k;
+            zpl[k] = ring + (j >= NB ? j - NB : j) * plane_sz + me;
+        }
+        j0 = j0 + 1 == NB ? 0 : j0 + 1;
         double azn = 0.0;
         Trig trn;
         if (z + 1 < ze) {
@@ -377,10 +377,6 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
         }
         az = azn;
         tr = trn;
-#pragma unroll
-        for (int k = 0; k < 2 * W; ++k) zoff[k] = zoff[k + 1];
-        zoff[2 * W] = znext + me;
-        bump(znext, plane_sz, ring_sz);
         bump(vr_off, vplane_sz, vring_sz);
     }
     cp_async_wait<0>();
