@@ -328,6 +328,29 @@ def b200_arm(args):
         e2e_s = float(tt.item())
     e2e_value = nodes_total * stages * e2e_steps / e2e_s
 
+    # ---- e2e_leg: the reference's usage pattern, one stateless integrate()
+    # call over K steps (lsg_integrate: host field in, K steps, host field out)
+    import ctypes as C
+    lib = _lib.load()
+    nlog = e2e_steps + 8
+    log = (abi.LsgStepLog * nlog)()
+    nst, tfin = C.c_size_t(), C.c_double()
+    opts = abi.make_opts(max_step=dt)
+    leg = lambda: lib.lsg_integrate(ctx.h, C.byref(setup.grid), C.byref(setup.problem), C.c_int(setup.method),
+                                    C.c_double(0.0), C.c_double(e2e_steps * dt), pinned.ptr, C.byref(opts), log,
+                                    C.c_size_t(nlog), C.byref(nst), C.byref(tfin))
+    _lib.raise_for(leg())  # warm (builds the cached solver)
+    barrier()
+    t0 = time.perf_counter()
+    _lib.raise_for(leg())
+    barrier()
+    leg_s = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([leg_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        leg_s = float(tt.item())
+    leg_value = nodes_total * stages * nst.value / leg_s
+
     if rank != 0:
         return 0
 
@@ -395,6 +418,15 @@ def b200_arm(args):
             "d2h_bytes_per_step": 8 * nodes_local,
             "steps": e2e_steps,
             "path": "lsg_solver_set_field (pinned H2D) + lsg_solver_step + lsg_solver_get_field (pinned D2H)",
+        },
+        "e2e_leg": {
+            "value": leg_value,
+            "unit": UNIT,
+            "steps": nst.value,
+            "h2d_bytes_per_call": 8 * nodes_local,
+            "d2h_bytes_per_call": 8 * nodes_local,
+            "path": "one lsg_integrate call (the reference's integrate(term, {0, K*dt}, v0, {max_step}) usage, "
+                    "as timed by the reference arm): pinned host field in, K steps, host field out",
         },
         "clocks": sampler.summary(),
     }
