@@ -736,12 +736,41 @@ void exchange(lsg_solver* s, int b, cudaStream_t st) {
     NCCL_CHECK(ncclGroupEnd());
 }
 
-// zlo/zhi: plane range [zlo, zhi) of every slab (zhi < 0: up to the slab end,
-// measured from the end when zlo < 0 is not used).
+// Geometry, tables, alpha, clamp and flags of one slab (what every stage of
+// every kernel variant shares).
+StageParams slab_params(lsg_solver* s, const Slab& sl) {
+    const int D = s->D;
+    StageParams P{};
+    P.zlo = 0;
+    P.zhi = sl.nz;
+    P.plane = s->plane;
+    P.n_local = sl.nodes;
+    long long st = 1;
+    for (int d = 0; d < D; ++d) {
+        P.n[d] = d == D - 1 ? sl.nz : s->g.counts[d];
+        P.stride[d] = st;
+        st *= P.n[d];
+        P.bc[d] = bc_of(&s->g, d);
+        P.lc[d] = s->lc[d];
+        P.alpha[d] = s->alpha[d];
+        P.axis[d] = s->axis[d];
+        P.tcos[d] = s->tcos[d];
+        P.tsin[d] = s->tsin[d];
+    }
+    P.z0 = sl.z0;
+    P.nz_glob = s->g.counts[D - 1];
+    P.halo = s->halo_w > 0 ? 1 : 0;
+    P.restrict_update = s->p.restrict_update;
+    P.direction = s->p.direction;
+    std::memcpy(P.hp, s->p.params, sizeof P.hp);
+    P.flags = s->dflags.as<unsigned>();
+    return P;
+}
+
+// One stage kernel per slab on `stream`; `part` selects the planes (below).
 void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range,
                   int part, cudaStream_t stream) {
     lsg_ctx* ctx = s->ctx;
-    const int D = s->D;
     for (Slab& sl : s->slabs) {
         // part 0: all planes; 1: interior planes [W, nz-W) that need no ghost
         // planes; 2: both boundary bands [0, W) and [nz-W, nz) in one launch
@@ -755,37 +784,16 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
             zhi = 2 * W, zsplit = W, zskip = sl.nz - 2 * W;
         }
         {
-        StageParams P{};
+        StageParams P = slab_params(s, sl);
         P.zlo = zlo;
         P.zhi = zhi;
         P.zsplit = zsplit;
         P.zskip = zskip;
-        P.plane = s->plane;
         P.u = sl.f[ui];
         P.v0 = vi >= 0 ? sl.f[vi] : nullptr;
         P.out = sl.f[oi];
-        P.n_local = sl.nodes;
-        long long st = 1;
-        for (int d = 0; d < D; ++d) {
-            P.n[d] = d == D - 1 ? sl.nz : s->g.counts[d];
-            P.stride[d] = st;
-            st *= P.n[d];
-            P.bc[d] = bc_of(&s->g, d);
-            P.lc[d] = s->lc[d];
-            P.alpha[d] = s->alpha[d];
-            P.axis[d] = s->axis[d];
-            P.tcos[d] = s->tcos[d];
-            P.tsin[d] = s->tsin[d];
-        }
-        P.z0 = sl.z0;
-        P.nz_glob = s->g.counts[D - 1];
-        P.halo = s->halo_w > 0 ? 1 : 0;
         P.dt = dt;
         P.c = c;
-        P.restrict_update = s->p.restrict_update;
-        P.direction = s->p.direction;
-        std::memcpy(P.hp, s->p.params, sizeof P.hp);
-        P.flags = s->dflags.as<unsigned>();
         P.range = range;
         if (s->b3fn[mode][0]) {
             void* args[] = {&P};

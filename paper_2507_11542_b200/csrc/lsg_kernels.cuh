@@ -22,55 +22,63 @@ namespace lsg {
 
 using StageFn = void (*)(StageParams);
 
+// One node of a fused stage (hamiltonian.cpp:11-88 + integrator.cpp:58-85):
+// L/R per dimension, central costate, H, global-LF dissipation, clamp, and
+// the TVD-RK combination of MODE.  Returns the stage output at idx.
+template <int D, int S, int KIND, int MODE>
+__device__ __forceinline__ double stage_node(const StageParams& P, const double* u, const double* v0, double dt,
+                                             double c, long long idx, bool& bad) {
+    constexpr int W = SchemeWidth<S>::W;
+    int i[D], ix[D];
+    double x[D];
+    long long r = idx;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        if (d == D - 1) {
+            i[d] = (int)r;
+        } else {
+            const long long q = r / P.n[d];
+            i[d] = (int)(r - q * P.n[d]);
+            r = q;
+        }
+        ix[d] = (d == D - 1) ? P.z0 + i[d] : i[d];
+        x[d] = __ldg(P.axis[d] + ix[d]);
+    }
+    double p[D];
+    double diss = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        double s[2 * W + 1];
+        gather_window<W>(u, idx, i[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s);
+        double L, R;
+        line_lr<S>(s, P.lc[d], L, R);
+        p[d] = 0.5 * (L + R);              // hamiltonian.cpp:31-32
+        diss += P.alpha[d] * (R - L);       // hamiltonian.cpp:60-64
+    }
+    const double H = hamiltonian<KIND, D>(P, x, load_trig<KIND>(P, D > 2 ? ix[D > 2 ? 2 : 0] : 0, D > 5 ? ix[D > 5 ? 5 : 0] : 0), p);
+    bad |= !isfinite(H);                    // hamiltonian.cpp:38-40
+    double dv = -(H - 0.5 * diss);          // hamiltonian.cpp:65
+    if (P.restrict_update)                  // hamiltonian.cpp:78-88
+        dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
+    if constexpr (MODE == MODE_TERM) {
+        return dv;
+    } else if constexpr (MODE == MODE_EULER) {
+        return __ldg(u + idx) + dt * dv;
+    } else {
+        const double base = v0[idx];  // plain load: out may alias v0 (in-place RK update)
+        return base + c * ((__ldg(u + idx) + dt * dv) - base);
+    }
+}
+
 template <int D, int S, int KIND, int MODE>
 __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ StageParams P) {
-    constexpr int W = SchemeWidth<S>::W;
     const long long lidx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long idx = lidx >= (long long)P.zsplit * P.plane ? lidx + (long long)P.zskip * P.plane : lidx;
     unsigned long long kmin = ~0ull, kmax = 0ull;
     bool bad = false;
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
     if (lidx < (long long)P.zhi * P.plane) {
-        int i[D], ix[D];
-        double x[D];
-        long long r = idx;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            if (d == D - 1) {
-                i[d] = (int)r;
-            } else {
-                const long long q = r / P.n[d];
-                i[d] = (int)(r - q * P.n[d]);
-                r = q;
-            }
-            ix[d] = (d == D - 1) ? P.z0 + i[d] : i[d];
-            x[d] = __ldg(P.axis[d] + ix[d]);
-        }
-        double p[D];
-        double diss = 0.0;
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            double s[2 * W + 1];
-            gather_window<W>(P.u, idx, i[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s);
-            double L, R;
-            line_lr<S>(s, P.lc[d], L, R);
-            p[d] = 0.5 * (L + R);              // hamiltonian.cpp:31-32
-            diss += P.alpha[d] * (R - L);       // hamiltonian.cpp:60-64
-        }
-        const double H = hamiltonian<KIND, D>(P, x, load_trig<KIND>(P, D > 2 ? ix[D > 2 ? 2 : 0] : 0, D > 5 ? ix[D > 5 ? 5 : 0] : 0), p);
-        bad = !isfinite(H);                     // hamiltonian.cpp:38-40
-        double dv = -(H - 0.5 * diss);          // hamiltonian.cpp:65
-        if (P.restrict_update)                  // hamiltonian.cpp:78-88
-            dv = P.direction == LSG_GROW ? ((0.0 < dv) ? 0.0 : dv) : ((dv < 0.0) ? 0.0 : dv);
-        double o;
-        if constexpr (MODE == MODE_TERM) {
-            o = dv;
-        } else if constexpr (MODE == MODE_EULER) {
-            o = __ldg(P.u + idx) + P.dt * dv;
-        } else {
-            const double base = P.v0[idx];  // plain load: out may alias v0 (in-place RK update)
-            o = base + P.c * ((__ldg(P.u + idx) + P.dt * dv) - base);
-        }
+        const double o = stage_node<D, S, KIND, MODE>(P, P.u, P.v0, P.dt, P.c, idx, bad);
         P.out[idx] = o;
         kmin = kmax = order_key(o);
     }
