@@ -249,6 +249,14 @@ int lsg_solver_step_bound(lsg_solver* s, double t, double* bound);
 /* Enqueue one TVD-RK step of size dt from time t (integrator.cpp:58-85) on the
  * context stream, no host synchronisation. */
 int lsg_solver_step(lsg_solver* s, double t, double dt);
+/* One step with the field coming from host memory and the result going back
+ * to it (set_field + step + get_field in one call, the reference's
+ * integrate(term, {t, t+dt}, v0) with host vectors).  On a single-slab solver
+ * the copies are chunked along the last axis and overlapped with the stage
+ * kernels (bit-identical result; overlap needs page-locked buffers, e.g.
+ * lsg_host_alloc).  host_in and host_out may alias.  Returns when host_out is
+ * complete.  LSG_PIPE=0 disables the overlap. */
+int lsg_solver_step_host(lsg_solver* s, double t, double dt, const double* host_in, double* host_out);
 /* Same as lsg_solver_step, bracketed by CUDA events recorded on the context
  * stream before the step and after every stage; synchronises and returns the
  * device time of each stage (stage_ms[0..stages-1]) and of the whole step. */

@@ -29,6 +29,7 @@ EXPORTS = (
     "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
     "lsg_solver_set_field", "lsg_solver_get_field", "lsg_solver_set_field_device",
     "lsg_solver_field_device", "lsg_solver_init_shape", "lsg_solver_step_bound", "lsg_solver_step",
+    "lsg_solver_step_host",
     "lsg_solver_step_timed",
     "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
 )
@@ -277,6 +278,19 @@ class Solver:
 
     def step(self, t, dt):
         call("lsg_solver_step", self.h, C.c_double(t), C.c_double(dt))
+
+    def step_host(self, t, dt, v, out=None):
+        """One step from a host field to a host result, copies overlapped with
+        the kernels (lsg_solver_step_host).  `out` may be `v` (in place)."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        if v.size != self.local_nodes:
+            raise ValueError("step_host: field size does not match the solver's local node count")
+        if out is None:
+            out = np.empty(self.local_nodes, dtype=np.float64)
+        elif out.dtype != np.float64 or out.size != self.local_nodes or not out.flags.c_contiguous:
+            raise ValueError("step_host: out must be a contiguous float64 array of local_nodes values")
+        call("lsg_solver_step_host", self.h, C.c_double(t), C.c_double(dt), abi.dptr(v), abi.dptr(out))
+        return out
 
     def step_timed(self, t, dt):
         """One step with device timing: (per-stage ms list, whole-step ms)."""

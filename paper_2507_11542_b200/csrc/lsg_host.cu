@@ -385,10 +385,17 @@ struct lsg_solver {
     bool halo_ok[3] = {false, false, false};
     cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
     cudaStream_t side = nullptr;  // boundary bands, concurrent with the interior (slabs only)
+    cudaStream_t cin = nullptr, cout = nullptr;  // lsg_solver_step_host copy streams (created on first use)
+    std::vector<cudaEvent_t> pipe_ev;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr, ev_main = nullptr, ev_bnd = nullptr;
     ~lsg_solver() {
         if (comm) cudaStreamSynchronize(comm);  // halo traffic done before the buffers go back to the pool
         if (side) cudaStreamSynchronize(side);
+        for (cudaStream_t st : {cin, cout})
+            if (st) cudaStreamSynchronize(st);
+        for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
+        for (cudaStream_t st : {cin, cout})
+            if (st) cudaStreamDestroy(st);
         for (cudaEvent_t e : {ev_ready, ev_halo, ev_main, ev_bnd})
             if (e) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
@@ -767,14 +774,70 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
     return P;
 }
 
-// One stage kernel per slab on `stream`; `part` selects the planes (below).
+// One stage kernel over the logical planes [zlo, zhi) of slab `sl` (planes at
+// or past zsplit shifted by zskip) on `stream`.
+void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, double dt, double c,
+                   unsigned long long* range, int zlo, int zhi, int zsplit, int zskip, cudaStream_t stream) {
+    lsg_ctx* ctx = s->ctx;
+    StageParams P = slab_params(s, sl);
+    P.zlo = zlo;
+    P.zhi = zhi;
+    P.zsplit = zsplit;
+    P.zskip = zskip;
+    P.u = sl.f[ui];
+    P.v0 = vi >= 0 ? sl.f[vi] : nullptr;
+    P.out = sl.f[oi];
+    P.dt = dt;
+    P.c = c;
+    P.range = range;
+    if (s->b3fn[mode][0]) {
+        void* args[] = {&P};
+        const long long pl = s->plane;
+        CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->b3fn[mode][range ? 1 : 0]),
+                                    dim3(static_cast<unsigned>((pl + 255) / 256), static_cast<unsigned>(zhi - zlo)),
+                                    dim3(256), args, 0, stream));
+    } else if (s->m3fn[mode][0]) {
+        March3 M = sl.m3;
+        if (zhi - zlo < sl.nz)  // a partial range: chunks of >= 3 planes
+            M.nzc = std::max(1, std::min(M.nzc, (zhi - zlo) / 3));
+        if (zskip) M.nzc = 2;  // one chunk per band: none straddles the gap
+        const dim3 grid(sl.m3_grid.x, static_cast<unsigned>(M.nzc));
+        void* args[] = {&P, &M};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(static_cast<unsigned>(s->m3_threads));
+        cfg.dynamicSmemBytes = s->m3_smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL with the previous stage
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), args));
+    } else {
+        void* args[] = {&P};
+        const long long n = static_cast<long long>(zhi - zlo) * s->plane;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)((n + 255) / 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->fn[mode]), args));
+    }
+    ctx->note_launch();
+}
+
+// One stage kernel per slab on `stream`; `part` selects the planes:
+// 0: all planes; 1: interior planes [W, nz-W) that need no ghost planes;
+// 2: both boundary bands [0, W) and [nz-W, nz) in one launch (logical planes
+// [0, 2W) with a gap of nz-2W planes after W).
 void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range,
                   int part, cudaStream_t stream) {
-    lsg_ctx* ctx = s->ctx;
     for (Slab& sl : s->slabs) {
-        // part 0: all planes; 1: interior planes [W, nz-W) that need no ghost
-        // planes; 2: both boundary bands [0, W) and [nz-W, nz) in one launch
-        // (logical planes [0, 2W) with a gap of nz-2W planes after W)
         int zlo = 0, zhi = sl.nz, zsplit = 0, zskip = 0;
         const int W = s->halo_w;
         if (part == 1) {
@@ -783,57 +846,7 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
         } else if (part == 2 && sl.nz > 2 * W) {
             zhi = 2 * W, zsplit = W, zskip = sl.nz - 2 * W;
         }
-        {
-        StageParams P = slab_params(s, sl);
-        P.zlo = zlo;
-        P.zhi = zhi;
-        P.zsplit = zsplit;
-        P.zskip = zskip;
-        P.u = sl.f[ui];
-        P.v0 = vi >= 0 ? sl.f[vi] : nullptr;
-        P.out = sl.f[oi];
-        P.dt = dt;
-        P.c = c;
-        P.range = range;
-        if (s->b3fn[mode][0]) {
-            void* args[] = {&P};
-            const long long pl = s->plane;
-            CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->b3fn[mode][range ? 1 : 0]),
-                                        dim3(static_cast<unsigned>((pl + 255) / 256), static_cast<unsigned>(zhi - zlo)),
-                                        dim3(256), args, 0, stream));
-        } else if (s->m3fn[mode][0]) {
-            March3 M = sl.m3;
-            if (zhi - zlo < M.nzc) M.nzc = zhi - zlo;
-            if (zskip) M.nzc = 2;  // one chunk per band: none straddles the gap
-            const dim3 grid(sl.m3_grid.x, static_cast<unsigned>(M.nzc));
-            void* args[] = {&P, &M};
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = grid;
-            cfg.blockDim = dim3(static_cast<unsigned>(s->m3_threads));
-            cfg.dynamicSmemBytes = s->m3_smem;
-            cfg.stream = stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL with the previous stage
-            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), args));
-        } else {
-            void* args[] = {&P};
-            const long long n = static_cast<long long>(zhi - zlo) * s->plane;
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)((n + 255) / 256));
-            cfg.blockDim = dim3(256);
-            cfg.stream = stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->fn[mode]), args));
-        }
-        ctx->note_launch();
-        }
+        launch_planes(s, sl, mode, ui, vi, oi, dt, c, range, zlo, zhi, zsplit, zskip, stream);
     }
 }
 
@@ -1054,6 +1067,129 @@ void download(lsg_solver* s, double* host, int b) {
                                        sizeof(double) * sl.nodes, cudaMemcpyDeviceToHost, ctx->stream));
     }
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+}
+
+// One step with the field coming from and going back to host memory, the
+// copies overlapped with the stage kernels (lsg_solver_step_host).  The input
+// is uploaded in K chunks of planes along the last axis on a copy-in stream.
+// After each chunk, every RK level computes every plane whose (2W+1)-plane
+// stencil of the previous level is available (periodic wrap or clamped
+// edge rule of the slab axis, as the kernels apply it), one launch per
+// contiguous run.  Each run of finished planes goes back on a copy-out
+// stream while later chunks are still arriving.  A plane's value is computed
+// by the same kernels from the same inputs, so the result is bit-identical to
+// upload + lsg_solver_step + download.  In-place RK updates are safe: level S
+// writes plane z of the input buffer only after every reader of that plane
+// (stage-1 stencils within W, the RK base at z) has run.
+void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* hout, unsigned long long* range) {
+    lsg_ctx* ctx = s->ctx;
+    Slab& sl = s->slabs[0];
+    const int nz = sl.nz, W = s->W;
+    const long long plane = s->plane;
+    const bool periodic = bc_of(&s->g, s->D - 1) == LSG_BC_PERIODIC;
+    const int S = stages_of(s->method);
+    int K = std::max(2, std::min(4, nz / (4 * W + 2)));
+    if (const char* e = std::getenv("LSG_PIPE_K")) K = std::max(2, std::min(16, std::atoi(e)));
+    if (!s->cin) {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s->cin, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s->cout, cudaStreamNonBlocking));
+    }
+    while (static_cast<int>(s->pipe_ev.size()) < K + 2) {
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s->pipe_ev.push_back(e);
+    }
+    cudaEvent_t ev_start = s->pipe_ev[K], ev_done = s->pipe_ev[K + 1];
+    // level l reads u = ob[l-1], writes ob[l] (integrator.cpp:58-85 buffer use)
+    const int a = s->cur;
+    int ob[4] = {a, 0, 0, 0}, mode[4] = {0, MODE_EULER, MODE_COMBINE, MODE_COMBINE}, v0b[4] = {-1, -1, a, a};
+    double cw[4] = {0.0, 0.0, 0.0, 0.0};
+    if (s->method == LSG_CFL1) {
+        ob[1] = 1 - a;
+    } else if (s->method == LSG_CFL2) {
+        ob[1] = 1 - a, ob[2] = a, cw[2] = 0.5;
+    } else {
+        ob[1] = (a + 1) % 3, ob[2] = (a + 2) % 3, ob[3] = a, cw[2] = 0.25, cw[3] = 2.0 / 3.0;
+    }
+    CUDA_CHECK(cudaEventRecord(ev_start, ctx->stream));  // earlier work on the buffers is done first
+    CUDA_CHECK(cudaStreamWaitEvent(s->cin, ev_start, 0));
+    // LSG_PIPE_TRACE=1: %globaltimer stamps after every upload chunk, compute
+    // round and copy-out batch, printed relative to the step start (tuning aid)
+    const bool trace = std::getenv("LSG_PIPE_TRACE") != nullptr;
+    std::vector<std::string> tnames;
+    unsigned long long* tbuf = nullptr;
+    if (trace) CUDA_CHECK(cudaMallocAsync(&tbuf, 64 * sizeof(unsigned long long), ctx->stream));
+    auto mark = [&](const std::string& what, cudaStream_t st) {
+        if (!trace || tnames.size() >= 64) return;
+        if (st != ctx->stream) {
+            CUDA_CHECK(cudaEventRecord(ev_done, ctx->stream));  // tbuf allocated
+            CUDA_CHECK(cudaStreamWaitEvent(st, ev_done, 0));
+        }
+        launch_stamp(tbuf + tnames.size(), st);
+        tnames.push_back(what);
+    };
+    mark("start", s->cin);
+    std::vector<int> cut(K + 1);
+    for (int j = 0; j <= K; ++j) cut[j] = static_cast<int>(static_cast<long long>(nz) * j / K);
+    for (int j = 0; j < K; ++j) {
+        CUDA_CHECK(cudaMemcpyAsync(sl.f[a] + cut[j] * plane, hin + cut[j] * plane,
+                                   sizeof(double) * static_cast<size_t>((cut[j + 1] - cut[j]) * plane),
+                                   cudaMemcpyHostToDevice, s->cin));
+        CUDA_CHECK(cudaEventRecord(s->pipe_ev[j], s->cin));
+        mark("h2d chunk " + std::to_string(j), s->cin);
+    }
+    std::vector<std::vector<char>> done(S + 1, std::vector<char>(nz, 0));
+    auto ready = [&](int l, int z) {
+        for (int k = -W; k <= W; ++k) {
+            int zz = z + k;
+            if (periodic) zz = ((zz % nz) + nz) % nz;
+            else zz = std::max(0, std::min(nz - 1, zz));
+            if (!done[l - 1][zz]) return false;
+        }
+        return true;
+    };
+    for (int j = 0; j < K; ++j) {
+        for (int z = cut[j]; z < cut[j + 1]; ++z) done[0][z] = 1;
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->pipe_ev[j], 0));
+        std::vector<std::pair<int, int>> final_runs;
+        for (int l = 1; l <= S; ++l) {
+            for (int z = 0; z < nz;) {
+                if (done[l][z] || !ready(l, z)) {
+                    ++z;
+                    continue;
+                }
+                int e = z;
+                while (e < nz && !done[l][e] && ready(l, e)) ++e;
+                launch_planes(s, sl, mode[l], ob[l - 1], v0b[l], ob[l], dt, cw[l], l == S ? range : nullptr, z, e, 0,
+                              0, ctx->stream);
+                for (int q = z; q < e; ++q) done[l][q] = 1;
+                if (l == S) final_runs.emplace_back(z, e);
+                z = e;
+            }
+        }
+        mark("compute round " + std::to_string(j), ctx->stream);
+        if (!final_runs.empty()) {
+            CUDA_CHECK(cudaEventRecord(ev_done, ctx->stream));
+            CUDA_CHECK(cudaStreamWaitEvent(s->cout, ev_done, 0));
+            for (const auto& r : final_runs)
+                CUDA_CHECK(cudaMemcpyAsync(hout + r.first * plane, sl.f[ob[S]] + r.first * plane,
+                                           sizeof(double) * static_cast<size_t>((r.second - r.first) * plane),
+                                           cudaMemcpyDeviceToHost, s->cout));
+            mark("d2h after round " + std::to_string(j), s->cout);
+        }
+    }
+    for (int z = 0; z < nz; ++z)
+        if (!done[S][z]) fail(LSG_ECUDA, "step_host: pipeline left planes unscheduled");
+    CUDA_CHECK(cudaStreamSynchronize(s->cout));
+    s->cur = ob[S];
+    if (trace) {
+        std::vector<unsigned long long> t(tnames.size());
+        CUDA_CHECK(cudaDeviceSynchronize());
+        CUDA_CHECK(cudaMemcpy(t.data(), tbuf, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
+        CUDA_CHECK(cudaFree(tbuf));
+        for (size_t k = 0; k < t.size(); ++k)
+            std::fprintf(stderr, "pipe %-22s %8.1f us\n", tnames[k].c_str(), 1e-3 * static_cast<double>(t[k] - t[0]));
+    }
 }
 
 }  // namespace
@@ -1654,6 +1790,29 @@ int lsg_solver_step(lsg_solver* s, double t, double dt) {
         if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
         enqueue_step(s, dt, s->drange.as<unsigned long long>() + 2 * s->ring_next);
         ++s->ring_next;
+    });
+}
+
+int lsg_solver_step_host(lsg_solver* s, double t, double dt, const double* host_in, double* host_out) {
+    (void)t;
+    return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!host_in || !host_out) fail(LSG_EINVAL, "step_host: null host buffer");
+        activate(s->ctx);
+        check_alpha_valid(s);
+        if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
+        unsigned long long* range = s->drange.as<unsigned long long>() + 2 * s->ring_next;
+        ++s->ring_next;
+        const char* e = std::getenv("LSG_PIPE");
+        const bool pipe = !(e && std::string(e) == "0");
+        if (pipe && s->slabs.size() == 1 && !s->distributed && s->halo_w == 0 && s->slabs[0].nz >= 2 * (4 * s->W + 2)) {
+            invalidate_halos(s);
+            step_host_pipelined(s, dt, host_in, host_out, range);
+        } else {  // several slabs or ranks, or too few planes to pipeline
+            upload(s, host_in, s->cur);
+            enqueue_step(s, dt, range);
+            download(s, host_out, s->cur);
+        }
     });
 }
 

@@ -150,3 +150,12 @@ void launch_range_init(unsigned long long* r, long long nslots, cudaStream_t st)
 }
 
 }  // namespace lsg
+
+namespace lsg {
+__global__ void stamp_kernel(unsigned long long* out) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *out = t;
+}
+void launch_stamp(unsigned long long* out, cudaStream_t st) { stamp_kernel<<<1, 1, 0, st>>>(out); }
+}  // namespace lsg

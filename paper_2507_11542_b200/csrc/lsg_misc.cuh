@@ -54,6 +54,7 @@ void launch_shift(const double* padded, double* out, long long N, int n, long lo
                   cudaStream_t st);
 void launch_restrict(const double* in, double* out, long long n, int direction, cudaStream_t st);
 void launch_shape(const ShapeParams& S, cudaStream_t st);
+void launch_stamp(unsigned long long* out, cudaStream_t st);  // %globaltimer into *out (tracing)
 void launch_range_init(unsigned long long* r, long long nslots, cudaStream_t st);
 long long zero_set_2d(const double* f, int nx, int ny, const double* ax, const double* ay, double dx, double dy,
                       double* seg_dev, long long cap, int* scratch_counts, int* scratch_offsets, void* temp,
