@@ -755,6 +755,7 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
     long long st = 1;
     for (int d = 0; d < D; ++d) {
         P.n[d] = d == D - 1 ? sl.nz : s->g.counts[d];
+        P.inv_n[d] = 1.0 / P.n[d];
         P.stride[d] = st;
         st *= P.n[d];
         P.bc[d] = bc_of(&s->g, d);

@@ -37,9 +37,7 @@ __device__ __forceinline__ double stage_node(const StageParams& P, const double*
         if (d == D - 1) {
             i[d] = (int)r;
         } else {
-            const long long q = r / P.n[d];
-            i[d] = (int)(r - q * P.n[d]);
-            r = q;
+            r = divmod_index(r, P.n[d], P.inv_n[d], i[d]);
         }
         ix[d] = (d == D - 1) ? P.z0 + i[d] : i[d];
         x[d] = __ldg(P.axis[d] + ix[d]);
