@@ -35,3 +35,15 @@ def test_cpp_dropin_reference_benchmark_outputs():
     assert set(got) == set(want)
     bad = {k: (got[k], want[k]) for k in want if got[k] != want[k]}
     assert not bad, bad
+
+
+def test_divmod_index_exact():
+    """The generic kernel's index decomposition (divmod_index, lsg_device.cuh)
+    equals exact 64-bit integer division on ~1e8 inputs up to 2^40, dense
+    around multiples of every divisor 1..65536 (tests/cpp/divmod_check.cu)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    binary = os.path.join(root, "tests", "cpp", "divmod_check")
+    assert os.path.exists(binary), "tests/cpp/divmod_check not built: run __graft_entry__.build()"
+    out = subprocess.run([binary], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "divmod ok" in out.stdout
