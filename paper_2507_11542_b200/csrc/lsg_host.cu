@@ -646,6 +646,14 @@ lsg_solver* cached_solver(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p,
     return ctx->cached;
 }
 
+// Before a collective on the main stream: the halo exchange last issued on the
+// communication stream (the one that follows a stage's boundary bands) is
+// complete, so the communicator's operations run in one order on every rank
+// whatever the library's cross-stream ordering.
+void join_comm(lsg_solver* s) {
+    if (s->comm && s->ev_halo) CUDA_CHECK(cudaStreamWaitEvent(s->ctx->stream, s->ev_halo, 0));
+}
+
 void ensure_range(lsg_solver* s, long long nslots) {
     if (s->range_cap < nslots) {
         s->drange.alloc(sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots), s->ctx->stream);
@@ -683,8 +691,10 @@ void ensure_alpha(lsg_solver* s) {
                                     dim3(256), args, 0, ctx->stream));
         ctx->note_launch();
     }
-    if (s->distributed)
+    if (s->distributed) {
+        join_comm(s);
         NCCL_CHECK(ncclAllReduce(s->dalpha.p, s->dalpha.p, 8, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    }
     unsigned long long keys[8];
     CUDA_CHECK(cudaMemcpyAsync(keys, s->dalpha.p, sizeof keys, cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -1004,6 +1014,7 @@ void run_leg(lsg_solver* s, LegPlan& plan) {
     for (long long k = 0; k < nsteps; ++k) enqueue_step(s, log[k].dt, s->drange.as<unsigned long long>() + 2 * k);
     unsigned flags = 0;
     if (s->distributed) {
+        join_comm(s);
         NCCL_CHECK(ncclAllReduce(s->dflags.p, s->dflags.p, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
         if (nsteps)  // both slots are max-reduced: {~min key, max key} per step
             NCCL_CHECK(ncclAllReduce(s->drange.p, s->drange.p, static_cast<size_t>(2 * nsteps), ncclUint64, ncclMax,
