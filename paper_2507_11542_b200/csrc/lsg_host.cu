@@ -627,6 +627,15 @@ std::string solver_key(const lsg_grid* g, const lsg_problem* p, int method) {
     return k;
 }
 
+void drop_cached(lsg_ctx* ctx) noexcept {  // also runs from a scope guard: never throws
+    if (ctx->cached) {
+        cudaStreamSynchronize(ctx->stream);
+        delete ctx->cached;
+    }
+    ctx->cached = nullptr;
+    ctx->cached_key.clear();
+}
+
 lsg_solver* cached_solver(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int method) {
     activate(ctx);
     check_grid(g);
@@ -638,12 +647,37 @@ lsg_solver* cached_solver(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p,
         ctx->cached->cur = 0;
         return ctx->cached;
     }
-    delete ctx->cached;  // release its device memory before allocating the next
-    ctx->cached = nullptr;
-    ctx->cached_key.clear();
+    drop_cached(ctx);  // release its device memory before allocating the next
     ctx->cached = make_solver(ctx, g, p, method, 1).release();
-    ctx->cached_key = enabled ? std::move(key) : std::string("\x01disabled");
+    // large solvers are not kept: their buffers would crowd out the caller's own
+    // allocations (CallCache drops them when the call returns)
+    long long max_bytes = 2LL << 30;
+    if (const char* e = std::getenv("LSG_CALL_CACHE_MAX_BYTES")) max_bytes = std::atoll(e);
+    const long long bytes = static_cast<long long>(sizeof(double)) * ctx->cached->total * (method == LSG_CFL3 ? 3 : 2);
+    ctx->cached_key = (enabled && bytes <= max_bytes) ? std::move(key) : std::string("\x01not cached");
     return ctx->cached;
+}
+
+// Scope guard of a stateless call: a solver that is not to be kept (caching
+// disabled or too large) is released when the call returns, also on errors.
+struct CallCache {
+    lsg_ctx* ctx;
+    ~CallCache() {
+        if (ctx && ctx->cached && ctx->cached_key.rfind("\x01", 0) == 0) drop_cached(ctx);
+    }
+};
+
+// Build a solver; when the device is out of memory and the context still
+// holds a cached stateless-call solver, release that and retry once.
+std::unique_ptr<lsg_solver> make_solver_retry(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int method,
+                                              int nslabs) {
+    try {
+        return make_solver(ctx, g, p, method, nslabs);
+    } catch (const Error& e) {
+        if (e.code != LSG_ENOMEM || !ctx || !ctx->cached) throw;
+        drop_cached(ctx);
+        return make_solver(ctx, g, p, method, nslabs);
+    }
 }
 
 // Before a collective on the main stream: the halo exchange last issued on the
@@ -1576,6 +1610,7 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
     (void)t;
     return guarded([&] {
         lsg_solver* s = cached_solver(ctx, g, p, LSG_CFL1);
+        CallCache call_cache{ctx};
         if (!s->invalid.empty()) fail(LSG_EINVAL, s->invalid);
         upload(s, v, 0);
         ensure_alpha(s);
@@ -1612,6 +1647,7 @@ int lsg_integrate(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int met
     return guarded([&] {
         if (opts) check_options(opts);
         lsg_solver* s = cached_solver(ctx, g, p, method);
+        CallCache call_cache{ctx};
         LegPlan plan = plan_leg(s, t0, tf, opts);
         check_log_room(plan.log.size(), steps, log_cap, n_steps);
         upload(s, v, 0);
@@ -1641,6 +1677,7 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
         if (integration_seconds) *integration_seconds = 0.0;
         if (duration == 0.0 || n_checkpoints == 1) return;
         lsg_solver* s = cached_solver(ctx, g, p, method);
+        CallCache call_cache{ctx};
         const int segments = n_checkpoints - 1;
         // every leg's schedule up front (reachability.cpp:160-170: the next leg
         // starts from leg.t), so the log capacity is known before device work
@@ -1676,7 +1713,7 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
 
 int lsg_solver_create(lsg_ctx* ctx, const lsg_grid* global_grid, const lsg_problem* p, int method,
                       lsg_solver** out) {
-    return guarded([&] { *out = make_solver(ctx, global_grid, p, method, 1).release(); });
+    return guarded([&] { *out = make_solver_retry(ctx, global_grid, p, method, 1).release(); });
 }
 
 int lsg_solver_create_slabs(lsg_ctx* ctx, const lsg_grid* global_grid, const lsg_problem* p, int method, int nslabs,
@@ -1685,7 +1722,7 @@ int lsg_solver_create_slabs(lsg_ctx* ctx, const lsg_grid* global_grid, const lsg
         if (!ctx) fail(LSG_EINVAL, "null context");
         if (ctx->nranks > 1) fail(LSG_EINVAL, "in-process slabs need a single-rank context");
         if (nslabs < 1) fail(LSG_EINVAL, "nslabs must be >= 1");
-        *out = make_solver(ctx, global_grid, p, method, nslabs).release();
+        *out = make_solver_retry(ctx, global_grid, p, method, nslabs).release();
     });
 }
 

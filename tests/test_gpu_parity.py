@@ -458,3 +458,28 @@ def test_slice_2d_matches_reference(ctx, port, ref):
         assert_bitwise(out, r, f"slice {fixed}={idx}")
     with pytest.raises(ValueError):
         ctx.slice_2d(S.grid, v, 2, 21)
+
+
+def test_stateless_call_cache_limits(ctx, port, monkeypatch):
+    """Stateless calls (term, integrate) give identical results whether their
+    solver is cached, too large to cache (released when the call returns), or
+    caching is off; a solver built afterwards is unaffected."""
+    S = P.cfg2_air3d(21)
+    v0 = H.initial_value(port, S)
+    want_t, want_b = port.term_lf(S.grid, S.problem, 0.0, v0)
+    for env in [{}, {"LSG_CALL_CACHE_MAX_BYTES": "1"}, {"LSG_CALL_CACHE": "0"}]:
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        for _ in range(2):
+            a, b = ctx.term_lf(S.grid, S.problem, 0.0, v0)
+            assert b == want_b
+            assert_bitwise(a, want_t, f"term {env}")
+            va, sa, _ = ctx.integrate(S.grid, S.problem, S.method, 0.0, 0.05, v0)
+            vb, sb, _ = port.integrate(S.grid, S.problem, S.method, 0.0, 0.05, v0)
+            assert_bitwise(va, vb, f"integrate {env}")
+        for k in env:
+            monkeypatch.delenv(k)
+    s = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    s.set_field(v0)
+    s.integrate(0.0, 0.05)
+    assert_bitwise(s.get_field(), vb, "solver after stateless calls")
