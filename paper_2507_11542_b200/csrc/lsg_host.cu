@@ -474,20 +474,35 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     int TX = 0, R = 0;
     if (s->invalid.empty() && s->D == 3 && !force_generic() && !s->b3fn[0][0]) {
         const int n0 = g->counts[0], n1 = g->counts[1];
-        if (n0 <= 256) {
-            TX = (n0 + 1) & ~1;  // full rows
-            R = std::max(1, 256 / (TX / 2));
-        } else {
-            TX = 32;
-            R = 16;
-        }
-        if (const char* e = std::getenv("LSG_M3_R")) R = std::max(1, std::atoi(e));
-        R = std::min(R, n1);
         const int W = s->W;
-        const int threads = ((TX / 2 * R + 31) / 32) * 32;
-        const int halo = 2 * W * std::min(TX, n0) + 2 * W * R;
+        // tile shapes in order of preference: full rows (no x halo), then x
+        // segments; the first that fits 256 threads and kMaxHalo halo slots
+        // per thread wins (full rows of more than ~120 nodes leave too few
+        // rows per tile for the halo budget)
+        std::vector<std::pair<int, int>> shapes;
+        if (n0 <= 256) shapes.emplace_back((n0 + 1) & ~1, std::max(1, 256 / (((n0 + 1) & ~1) / 2)));
+        shapes.emplace_back(32, 16);
+        shapes.emplace_back(64, 8);
+        if (const char* e = std::getenv("LSG_M3_TX")) {  // tuning override
+            const int tx = std::max(2, std::atoi(e) & ~1);
+            shapes.insert(shapes.begin(), {tx, std::max(1, 256 / (tx / 2))});
+        }
+        int threads = 0, halo = 0;
+        bool fits = false;
+        for (const auto& sh : shapes) {
+            TX = sh.first;
+            R = sh.second;
+            if (const char* e = std::getenv("LSG_M3_R")) R = std::max(1, std::atoi(e));
+            R = std::min(R, n1);
+            threads = ((TX / 2 * R + 31) / 32) * 32;
+            halo = 2 * W * std::min(TX, n0) + 2 * W * R;
+            if (threads <= 256 && halo <= kMaxHalo * threads) {
+                fits = true;
+                break;
+            }
+        }
         const long long padded_nodes = static_cast<long long>(g->counts[2] + 2 * W) * n0 * n1;
-        if (threads <= 256 && halo <= kMaxHalo * threads && padded_nodes < (1LL << 31) - 1) {
+        if (fits && padded_nodes < (1LL << 31) - 1) {
             bool all = true;
             for (int m = 0; m < 3; ++m)
                 for (int r = 0; r < 2; ++r) {

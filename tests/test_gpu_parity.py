@@ -298,6 +298,8 @@ def test_cfg5_full_size_properties(ctx):
     ((257, 13, 11), (1,)),         # ragged last x tile (1 column), periodic y only
     ((7, 300, 8), (0, 2)),         # tiny rows: many rows per tile, full-row periodic wrap
     ((33, 7, 7), ()),              # minimum stencil room along y and z
+    ((160, 9, 8), (0,)),           # rows too long for full-row tiles: 32-wide segments
+    ((250, 11, 7), (2,)),          # ... ragged last segment
 ])
 def test_march3_tilings_vs_oracle(ctx, port, counts, periodic):
     """The 2.5-D tiled 3-D kernel on awkward shapes, all schemes, bit for bit."""

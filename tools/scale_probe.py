@@ -9,7 +9,7 @@ ctx = _lib.Context(0)
 for kern in ["march3", "generic"]:
     if kern == "generic":
         os.environ["LSG_KERNEL"] = "generic"
-    for n in [48, 64, 101, 128, 160, 200, 256]:
+    for n in [int(a) for a in os.environ.get("SIZES", "48,64,101,128,160,200,256").split(",")]:
         S = P.cfg2_air3d(n)
         s = _lib.Solver(ctx, S.grid, S.problem, S.method)
         s.init_shape(*S.ic[:3], S.ic[3])
