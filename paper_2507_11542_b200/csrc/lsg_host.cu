@@ -1769,6 +1769,8 @@ int lsg_solver_slab(const lsg_solver* s, int* z0, int* nz, size_t* local_nodes) 
 
 int lsg_solver_set_field(lsg_solver* s, const double* host_v) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!host_v) fail(LSG_EINVAL, "set_field: null host buffer");
         activate(s->ctx);
         s->cur = 0;
         upload(s, host_v, 0);
@@ -1778,6 +1780,8 @@ int lsg_solver_set_field(lsg_solver* s, const double* host_v) {
 
 int lsg_solver_get_field(lsg_solver* s, double* host_v) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!host_v) fail(LSG_EINVAL, "get_field: null host buffer");
         activate(s->ctx);
         download(s, host_v, s->cur);
     });
@@ -1785,6 +1789,8 @@ int lsg_solver_get_field(lsg_solver* s, double* host_v) {
 
 int lsg_solver_set_field_device(lsg_solver* s, const double* dev_v) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!dev_v) fail(LSG_EINVAL, "set_field_device: null device pointer");
         activate(s->ctx);
         s->cur = 0;
         invalidate_halos(s);
@@ -1798,6 +1804,8 @@ int lsg_solver_set_field_device(lsg_solver* s, const double* dev_v) {
 
 int lsg_solver_field_device(lsg_solver* s, double** dev_v) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!dev_v) fail(LSG_EINVAL, "field_device: null output");
         if (s->slabs.size() != 1) fail(LSG_EINVAL, "field_device: solver holds several slabs");
         *dev_v = s->slabs[0].f[s->cur];
         invalidate_halos(s);  // the caller may write through the pointer
@@ -1806,6 +1814,7 @@ int lsg_solver_field_device(lsg_solver* s, double** dev_v) {
 
 int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const double* center, double radius) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
         activate(s->ctx);
         if (shape < 0 || shape > 2) fail(LSG_EINVAL, "init_shape: unknown shape");
         if (!(radius > 0.0)) fail(LSG_EINVAL, "init_shape: radius must be positive");
@@ -1841,6 +1850,8 @@ int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const
 int lsg_solver_step_bound(lsg_solver* s, double t, double* bound) {
     (void)t;
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!bound) fail(LSG_EINVAL, "step_bound: null output");
         activate(s->ctx);
         check_alpha_valid(s);
         *bound = s->bound;
@@ -1850,6 +1861,7 @@ int lsg_solver_step_bound(lsg_solver* s, double t, double* bound) {
 int lsg_solver_step(lsg_solver* s, double t, double dt) {
     (void)t;
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
         check_alpha_valid(s);
         if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
         enqueue_step(s, dt, s->drange.as<unsigned long long>() + 2 * s->ring_next);
@@ -1883,6 +1895,8 @@ int lsg_solver_step_host(lsg_solver* s, double t, double dt, const double* host_
 int lsg_solver_step_timed(lsg_solver* s, double t, double dt, double* stage_ms, double* step_ms) {
     (void)t;
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!stage_ms || !step_ms) fail(LSG_EINVAL, "step_timed: null output");
         activate(s->ctx);
         check_alpha_valid(s);
         if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
@@ -1907,6 +1921,7 @@ int lsg_solver_step_timed(lsg_solver* s, double t, double dt, double* stage_ms, 
 int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* opts, lsg_steplog* steps,
                          size_t log_cap, size_t* n_steps, double* t_final) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
         activate(s->ctx);
         LegPlan plan = plan_leg(s, t0, tf, opts);
         check_log_room(plan.log.size(), steps, log_cap, n_steps);
@@ -1918,6 +1933,8 @@ int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* op
 
 int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path) {
     return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        if (!path) fail(LSG_EINVAL, "write_snapshot: null path");
         activate(s->ctx);
         lsg_grid g = s->g;
         size_t n = static_cast<size_t>(s->total);
@@ -1938,14 +1955,18 @@ int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path) {
 }
 
 int lsg_solver_stream(lsg_solver* s, void** stream) {
-    return guarded([&] { *stream = reinterpret_cast<void*>(s->ctx->stream); });
+    return guarded([&] {
+        if (!s || !stream) fail(LSG_EINVAL, "stream: null argument");
+        *stream = reinterpret_cast<void*>(s->ctx->stream);
+    });
 }
 
 int lsg_solver_launches_per_step(const lsg_solver* s, int* n) {
     return guarded([&] {
-        int per_stage = 0;
+        if (!s || !n) fail(LSG_EINVAL, "launches_per_step: null argument");
+        int per_stage = 0;  // one launch, or boundary bands + interior (run_stage)
         for (const Slab& sl : s->slabs)
-            per_stage += s->halo_w == 0 ? 1 : (sl.nz > 2 * s->halo_w ? 3 : 1);
+            per_stage += s->halo_w == 0 ? 1 : (sl.nz > 2 * s->halo_w ? 2 : 1);
         *n = stages_of(s->method) * per_stage;
     });
 }

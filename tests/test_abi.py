@@ -79,3 +79,31 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("a CUDA device is present")
     with pytest.raises(RuntimeError, match="no CUDA device"):
         _lib.Context(0)
+
+
+def test_null_solver_handles_are_rejected():
+    """Every solver entry point returns LSG_EINVAL for a null handle (no crash,
+    no device needed)."""
+    lib = _lib.load()
+    d, p, n, sz = C.c_double(), C.c_void_p(), C.c_int(), C.c_size_t()
+    buf = (C.c_double * 4)()
+    calls = [
+        ("lsg_solver_set_field", (None, buf)),
+        ("lsg_solver_get_field", (None, buf)),
+        ("lsg_solver_set_field_device", (None, buf)),
+        ("lsg_solver_field_device", (None, C.byref(p))),
+        ("lsg_solver_init_shape", (None, 0, 0, None, C.c_double(1.0))),
+        ("lsg_solver_step_bound", (None, C.c_double(0.0), C.byref(d))),
+        ("lsg_solver_step", (None, C.c_double(0.0), C.c_double(0.01))),
+        ("lsg_solver_step_host", (None, C.c_double(0.0), C.c_double(0.01), buf, buf)),
+        ("lsg_solver_step_timed", (None, C.c_double(0.0), C.c_double(0.01), buf, buf)),
+        ("lsg_solver_integrate", (None, C.c_double(0.0), C.c_double(1.0), None, None, C.c_size_t(0), C.byref(sz),
+                                  C.byref(d))),
+        ("lsg_solver_write_snapshot", (None, C.c_double(0.0), b"/tmp/x")),
+        ("lsg_solver_stream", (None, C.byref(p))),
+        ("lsg_solver_launches_per_step", (None, C.byref(n))),
+        ("lsg_solver_slab", (None, C.byref(n), C.byref(n), C.byref(sz))),
+    ]
+    for name, args in calls:
+        assert getattr(lib, name)(*args) == abi.EINVAL, name
+    assert lib.lsg_solver_destroy(None) == abi.OK

@@ -503,3 +503,20 @@ def test_integrate_5d_6d_all_schemes(ctx, port, D, scheme):
         assert ta == tb
         assert_bitwise(sa, sb, f"steps D={D} s={scheme}")
         assert_bitwise(va, vb, f"v D={D} s={scheme}")
+
+
+@pytest.mark.parametrize("nslabs", [1, 2, 7])
+def test_launches_per_step_matches_counted_launches(ctx, nslabs):
+    """lsg_solver_launches_per_step equals the kernels a step actually launches
+    (one per stage, or boundary bands + interior per slab; thin slabs one)."""
+    import ctypes as C
+    S = P.cfg2_air3d(21)
+    s = _lib.Solver(ctx, S.grid, S.problem, S.method, nslabs=nslabs)
+    s.init_shape(*S.ic[:3], S.ic[3])
+    dt = 0.32 * s.step_bound()
+    s.step(0.0, dt)  # the first stage after a device write also exchanges halos
+    ctx.synchronize()
+    before = ctx.launches()
+    s.step(dt, dt)
+    ctx.synchronize()
+    assert ctx.launches() - before == s.launches_per_step()
