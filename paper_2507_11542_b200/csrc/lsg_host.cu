@@ -837,7 +837,8 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
 // One stage kernel over the logical planes [zlo, zhi) of slab `sl` (planes at
 // or past zsplit shifted by zskip) on `stream`.
 void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, double dt, double c,
-                   unsigned long long* range, int zlo, int zhi, int zsplit, int zskip, cudaStream_t stream) {
+                   unsigned long long* range, int zlo, int zhi, int zsplit, int zskip, cudaStream_t stream,
+                   int reserve_blocks = 0) {
     lsg_ctx* ctx = s->ctx;
     StageParams P = slab_params(s, sl);
     P.zlo = zlo;
@@ -860,6 +861,10 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         March3 M = sl.m3;
         if (zhi - zlo < sl.nz)  // a partial range: chunks of >= 3 planes
             M.nzc = std::max(1, std::min(M.nzc, (zhi - zlo) / 3));
+        if (reserve_blocks > 0) {  // share one wave with a concurrent launch (the boundary bands)
+            const int slots = 148 * s->m3_per_sm - reserve_blocks;
+            M.nzc = std::max(1, std::min(M.nzc, slots / std::max(1, static_cast<int>(sl.m3_grid.x))));
+        }
         if (zskip) M.nzc = 2;  // one chunk per band: none straddles the gap
         const dim3 grid(sl.m3_grid.x, static_cast<unsigned>(M.nzc));
         void* args[] = {&P, &M};
@@ -906,7 +911,9 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
         } else if (part == 2 && sl.nz > 2 * W) {
             zhi = 2 * W, zsplit = W, zskip = sl.nz - 2 * W;
         }
-        launch_planes(s, sl, mode, ui, vi, oi, dt, c, range, zlo, zhi, zsplit, zskip, stream);
+        // the interior runs beside the bands' launch (two chunks per tile)
+        const int reserve = part == 1 ? 2 * static_cast<int>(sl.m3_grid.x) : 0;
+        launch_planes(s, sl, mode, ui, vi, oi, dt, c, range, zlo, zhi, zsplit, zskip, stream, reserve);
     }
 }
 
