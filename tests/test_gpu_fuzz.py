@@ -17,6 +17,12 @@ pytestmark = pytest.mark.gpu
 
 MIN_NODES = {0: 3, 1: 5, 2: 7, 3: 7}
 
+# The default run replays a fixed case set (derandomized: the same cases on
+# every machine); LSG_FUZZ_RANDOM=1 LSG_FUZZ_EXAMPLES=N explores fresh ones.
+import os  # noqa: E402
+N_EXAMPLES = int(os.environ.get("LSG_FUZZ_EXAMPLES", "80"))
+DERANDOMIZE = os.environ.get("LSG_FUZZ_RANDOM") is None
+
 
 @st.composite
 def cases(draw):
@@ -40,7 +46,8 @@ def cases(draw):
     return D, scheme, counts, periodic, mins, spans, kind, params, clamp, direction, method, seed, nsteps
 
 
-@settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@settings(max_examples=N_EXAMPLES, deadline=None, derandomize=DERANDOMIZE,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(cases())
 def test_fuzz_integrate_bitwise(ctx, port, case):
     D, scheme, counts, periodic, mins, spans, kind, params, clamp, direction, method, seed, nsteps = case
@@ -81,7 +88,8 @@ def cases3(draw):
             draw(st.integers(1, 4)))
 
 
-@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+@settings(max_examples=(3 * N_EXAMPLES) // 4, deadline=None, derandomize=DERANDOMIZE,
+          suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(cases3())
 def test_fuzz_3d_kernels_and_slabs_bitwise(ctx, port, case):
     """Each 3-D kernel variant and a random slab count against the oracle."""
