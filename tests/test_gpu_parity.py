@@ -520,3 +520,22 @@ def test_launches_per_step_matches_counted_launches(ctx, nslabs):
     s.step(dt, dt)
     ctx.synchronize()
     assert ctx.launches() - before == s.launches_per_step()
+
+
+@pytest.mark.parametrize("scale", [1e-310, 1e-300, 3e-290])
+def test_weno5_exact_on_subnormal_differences(ctx, port, scale):
+    """Exact WENO5 on fields whose divided differences are subnormal or near
+    it: the constant divisions take the IEEE path there, bit for bit with the
+    reference arithmetic (upwind derivatives and a full LF term)."""
+    g = abi.make_grid([0.0, 0.0, 0.0], [1.0, 1.0, 1.0], [11, 9, 8], (1,))
+    v = H.random_field(g, 5) * scale
+    for d in range(3):
+        la, ra = ctx.upwind(g, v, d, abi.SCHEME_WENO5)
+        lb, rb = port.upwind(g, v, d, abi.SCHEME_WENO5)
+        assert_bitwise(la, lb, f"L dim {d}")
+        assert_bitwise(ra, rb, f"R dim {d}")
+    p = abi.make_problem(abi.HAM_NORMAL, abi.SCHEME_WENO5, [1.0], abi.GROW, False)
+    a, ba = ctx.term_lf(g, p, 0.0, v)
+    b, bb = port.term_lf(g, p, 0.0, v)
+    assert ba == bb
+    assert_bitwise(a, b, "term")

@@ -16,16 +16,25 @@ __device__ unsigned long long mix(unsigned long long z) {
 __global__ void check(unsigned long long seed, long long n, unsigned long long* bad, double* example) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         unsigned long long b = mix(seed + i);
-        // exponents between 2^-1000 and 2^1000 (no subnormal/overflow results), plus small integers
-        const int e = (int)((b >> 52) % 2001) - 1000;
-        b = (b & 0x800FFFFFFFFFFFFFull) | ((unsigned long long)(e + 1023) << 52);
+        // every exponent the fast path admits (div_const: x = 0 or |x| >= 2^-960;
+        // tinier operands take IEEE division in weno5_onesided), plus small
+        // integers and the special values
+        const unsigned long long be = 63 + (b >> 52) % (2047 - 63);
+        b = (b & 0x800FFFFFFFFFFFFFull) | (be << 52);
         double x = __longlong_as_double((long long)b);
         if ((i & 1023) == 0) x = (double)((long long)(b % 2001) - 1000);
         if (i == 0) x = -0.0;
         if (i == 1) x = 0.0;
+        if (i == 2) x = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+        if (i == 3) x = __longlong_as_double((long long)0xfff0000000000000ull);  // -inf
+        if (i == 4) x = __longlong_as_double(0x7ff8000000000000ll);   // NaN
+        if (i == 5) x = 0x1p-960;                                     // smallest admitted magnitude
+        if (i == 6) x = __longlong_as_double(0x7fefffffffffffffll);   // largest finite
         const double a3 = lsg::div_by3(x), r3 = x / 3.0;
         const double a6 = lsg::div_by6(x), r6 = x / 6.0;
-        if (__double_as_longlong(a3) != __double_as_longlong(r3) || __double_as_longlong(a6) != __double_as_longlong(r6)) {
+        const bool nan_ok = (x != x) && (a3 != a3) && (a6 != a6);  // NaN in, NaN out (payload not compared)
+        if (!nan_ok && (__double_as_longlong(a3) != __double_as_longlong(r3) ||
+                        __double_as_longlong(a6) != __double_as_longlong(r6))) {
             if (atomicAdd(bad, 1ull) == 0) *example = x;
         }
     }
