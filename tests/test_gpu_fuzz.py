@@ -43,23 +43,34 @@ def cases(draw):
     method = draw(st.integers(0, 2))
     seed = draw(st.integers(0, 2 ** 31))
     nsteps = draw(st.integers(1, 3))
-    return D, scheme, counts, periodic, mins, spans, kind, params, clamp, direction, method, seed, nsteps
+    scale = draw(st.sampled_from([1.0, 1.0, 1.0, 1e-200, 1e-305, 1e-312, 1e150]))  # incl. subnormal differences
+    return D, scheme, counts, periodic, mins, spans, kind, params, clamp, direction, method, seed, nsteps, scale
 
 
 @settings(max_examples=N_EXAMPLES, deadline=None, derandomize=DERANDOMIZE,
           suppress_health_check=[HealthCheck.function_scoped_fixture])
 @given(cases())
 def test_fuzz_integrate_bitwise(ctx, port, case):
-    D, scheme, counts, periodic, mins, spans, kind, params, clamp, direction, method, seed, nsteps = case
+    D, scheme, counts, periodic, mins, spans, kind, params, clamp, direction, method, seed, nsteps, scale = case
     g = abi.make_grid(mins, [m + s for m, s in zip(mins, spans)], counts, periodic)
     p = abi.make_problem(kind, scheme, params, direction, clamp)
-    v0 = H.random_field(g, seed)
-    _, bound = port.term_lf(g, p, 0.0, v0)
+    v0 = H.random_field(g, seed) * scale
+    try:
+        _, bound = port.term_lf(g, p, 0.0, v0)
+    except RuntimeError as e:  # e.g. overflowing |p|^2: the device must refuse the same way
+        with pytest.raises(RuntimeError, match=str(e).split(":")[0]):
+            ctx.term_lf(g, p, 0.0, v0)
+        return
     if not math.isfinite(bound):
         bound = 0.01
     tf = nsteps * 0.32 * bound * 0.999
+    try:
+        vb, sb, tb = port.integrate(g, p, method, 0.0, tf, v0)
+    except RuntimeError as e:
+        with pytest.raises(RuntimeError, match=str(e).split(":")[0]):
+            ctx.integrate(g, p, method, 0.0, tf, v0)
+        return
     va, sa, ta = ctx.integrate(g, p, method, 0.0, tf, v0)
-    vb, sb, tb = port.integrate(g, p, method, 0.0, tf, v0)
     assert ta == tb
     assert_bitwise(sa, sb, "step log")
     assert_bitwise(va, vb, "value function")
