@@ -96,7 +96,7 @@ def cases3(draw):
     return (scheme, (n0, n1, n2), periodic, kind, params, draw(st.booleans()),
             draw(st.sampled_from([abi.GROW, abi.SHRINK])), draw(st.integers(0, 2)),
             draw(st.integers(0, 2 ** 31)), draw(st.sampled_from(["march3", "box3", "generic"])),
-            draw(st.integers(1, 4)))
+            draw(st.integers(1, 4)), draw(st.sampled_from([1.0, 1.0, 1e-305, 1e-312])))
 
 
 @settings(max_examples=(3 * N_EXAMPLES) // 4, deadline=None, derandomize=DERANDOMIZE,
@@ -106,10 +106,10 @@ def test_fuzz_3d_kernels_and_slabs_bitwise(ctx, port, case):
     """Each 3-D kernel variant and a random slab count against the oracle."""
     import os
     from paper_2507_11542_b200 import _lib
-    scheme, counts, periodic, kind, params, clamp, direction, method, seed, kernel, nslabs = case
+    scheme, counts, periodic, kind, params, clamp, direction, method, seed, kernel, nslabs, scale = case
     g = abi.make_grid([-6.0, -10.0, 0.0], [20.0, 10.0, 6.0], list(counts), periodic)
     p = abi.make_problem(kind, scheme, params, direction, clamp)
-    v0 = H.random_field(g, seed, -3.0, 3.0)
+    v0 = H.random_field(g, seed, -3.0, 3.0) * scale
     _, bound = port.term_lf(g, p, 0.0, v0)
     tf = 2 * 0.32 * bound * 0.999 if math.isfinite(bound) else 0.01
     vb, sb, tb = port.integrate(g, p, method, 0.0, tf, v0)
