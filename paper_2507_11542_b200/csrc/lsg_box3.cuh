@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(256) box3_kernel(const __grid_constant__ Stage
     const int q = blockIdx.x * 256 + threadIdx.x;
     const int zl = P.zlo + blockIdx.y;
     const int z = zl >= P.zsplit ? zl + P.zskip : zl;
-    unsigned long long kmin = ~0ull, kmax = 0ull;
+    unsigned long long kmin = ~0ull, kmax = 0ull, fz = ~0ull;
     bool bad = false;
     if (q < plane) {
         const int y = q / n0, x = q - (q / n0) * n0;
@@ -67,36 +67,13 @@ __global__ void __launch_bounds__(256) box3_kernel(const __grid_constant__ Stage
             o = base + P.c * ((w0[W] + P.dt * dv) - base);
         }
         P.out[idx] = o;
-        if (RANGE) kmin = kmax = order_key(o);
+        if (RANGE) {
+            kmin = kmax = order_key(o);
+            fz = zero_code(o, (unsigned long long)((long long)P.z0 * plane + idx));
+        }
     }
     if (P.flags && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
-    if (RANGE && P.range) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-        }
-        __shared__ unsigned long long smin[8], smax[8];
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (lane == 0) {
-            smin[warp] = kmin;
-            smax[warp] = kmax;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            kmin = lane < 8 ? smin[lane] : ~0ull;
-            kmax = lane < 8 ? smax[lane] : 0ull;
-#pragma unroll
-            for (int off = 4; off > 0; off >>= 1) {
-                kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-                kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-            }
-            if (lane == 0) {
-                if (kmin != ~0ull) atomicMax(P.range, ~kmin);
-                if (kmax != 0ull) atomicMax(P.range + 1, kmax);
-            }
-        }
-    }
+    if (RANGE && P.range) block_range(P.range, kmin, kmax, fz);
 }
 
 using Box3Fn = void (*)(StageParams);

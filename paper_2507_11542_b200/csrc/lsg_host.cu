@@ -406,6 +406,8 @@ struct lsg_solver {
 namespace {
 
 constexpr long long kRingSlots = 4096;
+// per-step range slot: {~min key, max key, ~first zero code} (lsg_kernels.cuh block_range)
+constexpr long long kRangeWords = 3;
 
 void partition(int n, int P, int r, int* z0, int* nz) {
     const int base = n / P, rem = n % P;
@@ -606,7 +608,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->dflags.alloc(sizeof(unsigned) * 2, ctx->stream);
     s->dalpha.alloc(sizeof(unsigned long long) * 8, ctx->stream);
     CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, s->dflags.bytes, ctx->stream));
-    s->drange.alloc(sizeof(unsigned long long) * 2 * kRingSlots, ctx->stream);
+    s->drange.alloc(sizeof(unsigned long long) * kRangeWords * kRingSlots, ctx->stream);
     s->range_cap = kRingSlots;
     CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, s->drange.bytes, ctx->stream));
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // buffers usable from any stream from here on
@@ -705,10 +707,10 @@ void join_comm(lsg_solver* s) {
 
 void ensure_range(lsg_solver* s, long long nslots) {
     if (s->range_cap < nslots) {
-        s->drange.alloc(sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots), s->ctx->stream);
+        s->drange.alloc(sizeof(unsigned long long) * kRangeWords * static_cast<size_t>(nslots), s->ctx->stream);
         s->range_cap = nslots;
     }
-    CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, sizeof(unsigned long long) * 2 * static_cast<size_t>(nslots),
+    CUDA_CHECK(cudaMemsetAsync(s->drange.p, 0, sizeof(unsigned long long) * kRangeWords * static_cast<size_t>(nslots),
                                s->ctx->stream));
     s->ring_next = 0;
 }
@@ -1067,16 +1069,17 @@ void run_leg(lsg_solver* s, LegPlan& plan) {
     lsg_ctx* ctx = s->ctx;
     CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
     ensure_range(s, std::max<long long>(nsteps, 1));
-    for (long long k = 0; k < nsteps; ++k) enqueue_step(s, log[k].dt, s->drange.as<unsigned long long>() + 2 * k);
+    for (long long k = 0; k < nsteps; ++k)
+        enqueue_step(s, log[k].dt, s->drange.as<unsigned long long>() + kRangeWords * k);
     unsigned flags = 0;
     if (s->distributed) {
         join_comm(s);
         NCCL_CHECK(ncclAllReduce(s->dflags.p, s->dflags.p, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
         if (nsteps)  // both slots are max-reduced: {~min key, max key} per step
-            NCCL_CHECK(ncclAllReduce(s->drange.p, s->drange.p, static_cast<size_t>(2 * nsteps), ncclUint64, ncclMax,
+            NCCL_CHECK(ncclAllReduce(s->drange.p, s->drange.p, static_cast<size_t>(kRangeWords * nsteps), ncclUint64, ncclMax,
                                      ctx->comm, ctx->stream));
     }
-    std::vector<unsigned long long> keys(static_cast<size_t>(2 * nsteps));
+    std::vector<unsigned long long> keys(static_cast<size_t>(kRangeWords * nsteps));
     CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     if (nsteps)
         CUDA_CHECK(cudaMemcpyAsync(keys.data(), s->drange.p, sizeof(unsigned long long) * keys.size(),
@@ -1086,8 +1089,18 @@ void run_leg(lsg_solver* s, LegPlan& plan) {
         fail(LSG_ENUMERIC, "term_lax_friedrichs: hamiltonian produced a non-finite value");
     if (collapsed) fail(LSG_ENUMERIC, "integrator: step size collapsed to zero");
     for (long long k = 0; k < nsteps; ++k) {
-        log[k].v_min = key_to_double(~keys[2 * k]);
-        log[k].v_max = key_to_double(keys[2 * k + 1]);
+        const unsigned long long* w = keys.data() + kRangeWords * k;
+        double vmin = key_to_double(~w[0]), vmax = key_to_double(w[1]);
+        // +-0 share a key; integrator.cpp:87-90 keeps the first of equal values,
+        // i.e. the first zero in index order decides the sign (~w[2] = its code)
+        const unsigned long long fz = ~w[2];
+        if (fz != ~0ull) {
+            const double zero = (fz & 1ull) ? -0.0 : 0.0;
+            if (vmin == 0.0) vmin = zero;
+            if (vmax == 0.0) vmax = zero;
+        }
+        log[k].v_min = vmin;
+        log[k].v_max = vmax;
     }
 }
 
@@ -1871,7 +1884,7 @@ int lsg_solver_step(lsg_solver* s, double t, double dt) {
         if (!s) fail(LSG_EINVAL, "null solver");
         check_alpha_valid(s);
         if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
-        enqueue_step(s, dt, s->drange.as<unsigned long long>() + 2 * s->ring_next);
+        enqueue_step(s, dt, s->drange.as<unsigned long long>() + kRangeWords * s->ring_next);
         ++s->ring_next;
     });
 }
@@ -1884,7 +1897,7 @@ int lsg_solver_step_host(lsg_solver* s, double t, double dt, const double* host_
         activate(s->ctx);
         check_alpha_valid(s);
         if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
-        unsigned long long* range = s->drange.as<unsigned long long>() + 2 * s->ring_next;
+        unsigned long long* range = s->drange.as<unsigned long long>() + kRangeWords * s->ring_next;
         ++s->ring_next;
         const char* e = std::getenv("LSG_PIPE");
         const bool pipe = !(e && std::string(e) == "0");
@@ -1910,7 +1923,7 @@ int lsg_solver_step_timed(lsg_solver* s, double t, double dt, double* stage_ms, 
         const int n = stages_of(s->method);
         cudaEvent_t ev[4];
         for (int k = 0; k <= n; ++k) CUDA_CHECK(cudaEventCreate(&ev[k]));
-        enqueue_step(s, dt, s->drange.as<unsigned long long>() + 2 * s->ring_next, ev);
+        enqueue_step(s, dt, s->drange.as<unsigned long long>() + kRangeWords * s->ring_next, ev);
         ++s->ring_next;
         CUDA_CHECK(cudaEventSynchronize(ev[n]));
         for (int k = 0; k < n; ++k) {

@@ -22,6 +22,43 @@ namespace lsg {
 
 using StageFn = void (*)(StageParams);
 
+// Block reduction of a step's range candidates into its slot:
+// {~min key, max key, ~first zero code} (all max-reduced, also across ranks).
+__device__ __forceinline__ void block_range(unsigned long long* slot, unsigned long long kmin, unsigned long long kmax,
+                                            unsigned long long fz) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+        fz = min(fz, __shfl_xor_sync(0xffffffffu, fz, off));
+    }
+    __shared__ unsigned long long smin[32], smax[32], sfz[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        smin[warp] = kmin;
+        smax[warp] = kmax;
+        sfz[warp] = fz;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        kmin = lane < nw ? smin[lane] : ~0ull;
+        kmax = lane < nw ? smax[lane] : 0ull;
+        fz = lane < nw ? sfz[lane] : ~0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+            fz = min(fz, __shfl_xor_sync(0xffffffffu, fz, off));
+        }
+        if (lane == 0) {
+            if (kmin != ~0ull) atomicMax(slot, ~kmin);
+            if (kmax != 0ull) atomicMax(slot + 1, kmax);
+            if (fz != ~0ull) atomicMax(slot + 2, ~fz);
+        }
+    }
+}
+
 // One node of a fused stage (hamiltonian.cpp:11-88 + integrator.cpp:58-85):
 // L/R per dimension, central costate, H, global-LF dissipation, clamp, and
 // the TVD-RK combination of MODE.  Returns the stage output at idx.
@@ -72,45 +109,21 @@ template <int D, int S, int KIND, int MODE>
 __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ StageParams P) {
     const long long lidx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long idx = lidx >= (long long)P.zsplit * P.plane ? lidx + (long long)P.zskip * P.plane : lidx;
-    unsigned long long kmin = ~0ull, kmax = 0ull;
+    unsigned long long kmin = ~0ull, kmax = 0ull, fz = ~0ull;
     bool bad = false;
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // programmatic dependent launch
     if (lidx < (long long)P.zhi * P.plane) {
         const double o = stage_node<D, S, KIND, MODE>(P, P.u, P.v0, P.dt, P.c, idx, bad);
         P.out[idx] = o;
         kmin = kmax = order_key(o);
+        fz = zero_code(o, (unsigned long long)((long long)P.z0 * P.plane + idx));
     }
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     if (P.flags) {
         if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
     }
     if (P.range) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-        }
-        __shared__ unsigned long long smin[8], smax[8];
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        if (lane == 0) {
-            smin[warp] = kmin;
-            smax[warp] = kmax;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const int nw = blockDim.x >> 5;
-            kmin = lane < nw ? smin[lane] : ~0ull;
-            kmax = lane < nw ? smax[lane] : 0ull;
-#pragma unroll
-            for (int off = 4; off > 0; off >>= 1) {
-                kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-                kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-            }
-            if (lane == 0) {
-                if (kmin != ~0ull) atomicMax(P.range, ~kmin);  // slot 0 holds ~(min key)
-                if (kmax != 0ull) atomicMax(P.range + 1, kmax);
-            }
-        }
+        block_range(P.range, kmin, kmax, fz);
     }
 }
 

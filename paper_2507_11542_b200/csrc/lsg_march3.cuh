@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     for (int p = zs - W; p < zs + W; ++p) ghost_pass(p);
 
     unsigned long long kmin = ~0ull, kmax = 0ull;
+    unsigned fz = ~0u;  // first zero code (index << 1 | sign); padded grids < 2^31 nodes fit 32 bits
     bool bad = false;
     const double ax0 = __ldg(P.axis[0] + x), ax1 = __ldg(P.axis[0] + x + (two ? 1 : 0));
     const double ay = __ldg(P.axis[1] + y);
@@ -373,6 +374,11 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
                 const unsigned long long ka = order_key(oa), kb = two ? order_key(ob) : ka;
                 kmin = min(kmin, min(ka, kb));
                 kmax = max(kmax, max(ka, kb));
+                if (oa == 0.0 || (two && ob == 0.0)) {  // rare: zeros decide the step log's sign of 0
+                    const unsigned g = (unsigned)((P.z0 + z) * (int)s2 + coli);
+                    const unsigned ca = (unsigned)zero_code(oa, g), cb = two ? (unsigned)zero_code(ob, g + 1) : ~0u;
+                    fz = min(fz, min(ca, cb));
+                }
             }
         }
         az = azn;
@@ -383,34 +389,7 @@ __global__ void __launch_bounds__(256, 2) march3_kernel(const __grid_constant__ 
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     if (P.flags && __any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(P.flags, FLAG_HAM_NONFINITE);
-    if (RANGE && P.range) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-        }
-        __shared__ unsigned long long rmin[32], rmax[32];
-        const int warp = t >> 5, lane = t & 31;
-        if (lane == 0) {
-            rmin[warp] = kmin;
-            rmax[warp] = kmax;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            const int nw = blockDim.x >> 5;
-            kmin = lane < nw ? rmin[lane] : ~0ull;
-            kmax = lane < nw ? rmax[lane] : 0ull;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-                kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-            }
-            if (lane == 0) {
-                if (kmin != ~0ull) atomicMax(P.range, ~kmin);
-                if (kmax != 0ull) atomicMax(P.range + 1, kmax);
-            }
-        }
-    }
+    if (RANGE && P.range) block_range(P.range, kmin, kmax, fz == ~0u ? ~0ull : (unsigned long long)fz);
 }
 
 using March3Fn = void (*)(StageParams, March3);

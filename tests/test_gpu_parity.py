@@ -539,3 +539,31 @@ def test_weno5_exact_on_subnormal_differences(ctx, port, scale):
     b, bb = port.term_lf(g, p, 0.0, v)
     assert ba == bb
     assert_bitwise(a, b, "term")
+
+
+@pytest.mark.parametrize("kernel,counts,nslabs", [("march3", (21, 13, 11), 1), ("box3", (21, 13, 11), 1),
+                                                  ("march3", (21, 13, 11), 3), ("generic", (33, 29), 1)])
+@pytest.mark.parametrize("first_negative", [False, True])
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_step_log_signed_zero_extremes(ctx, port, monkeypatch, kernel, counts, nslabs, first_negative, sign):
+    """When a step's minimum (or maximum) is zero and the field holds both
+    +0.0 and -0.0, the step log reports the sign of the first zero in index
+    order, as the reference's sequential std::min/max does
+    (integrator.cpp:87-90).  Zero speed keeps the zeros through the stage."""
+    D = len(counts)
+    g = abi.make_grid([-1.0] * D, [1.0] * D, list(counts), (D - 1,))
+    p = abi.make_problem(abi.HAM_LINEAR, abi.SCHEME_ENO3, abi.linear_params([0.0] * D), abi.GROW, False)
+    v = sign * (1.0 + H.random_field(g, 3, 0.0, 1.0))
+    n = v.size
+    i, j = n // 3, 2 * n // 3
+    v[i], v[j] = (-0.0, 0.0) if first_negative else (0.0, -0.0)
+    if kernel != "march3":
+        monkeypatch.setenv("LSG_KERNEL", kernel)
+    for method in (abi.CFL1, abi.CFL2, abi.CFL3):
+        s = _lib.Solver(ctx, g, p, method, nslabs=nslabs)
+        s.set_field(v)
+        sa, ta = s.integrate(0.0, 0.1, abi.make_opts(max_step=0.05))
+        vb, sb, tb = port.integrate(g, p, method, 0.0, 0.1, v, abi.make_opts(max_step=0.05))
+        assert ta == tb
+        assert_bitwise(sa, sb, f"step log {kernel} m={method}")
+        assert_bitwise(s.get_field(), vb, f"field {kernel} m={method}")
