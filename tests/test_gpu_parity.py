@@ -448,6 +448,31 @@ def test_zero_set_matches_reference(ctx, port, ref, case):
     assert abs(length - rlen) <= 1e-12 * rlen
 
 
+@pytest.mark.parametrize("case", ["zero_lines", "sprinkled_signed_zeros", "all_zero"])
+def test_zero_set_exact_zero_nodes(ctx, port, ref, case):
+    """Marching squares with node values exactly +-0.0 (whole zero rows and
+    columns, scattered signed zeros, an all-zero field): same segments, order
+    and bits as contour.cpp:27-97."""
+    g = abi.make_grid([-1.0, -1.0], [1.0, 1.0], [21, 17])  # x = 0 and y = 0 are grid lines
+    x = np.array([port.axis(g, 0)[i] for i in range(21)])
+    y = np.array([port.axis(g, 1)[j] for j in range(17)])
+    X, Y = np.meshgrid(x, y, indexing="xy")  # column-major: index = i + 21 * j
+    if case == "zero_lines":
+        v = (X * Y).ravel()
+    elif case == "sprinkled_signed_zeros":
+        v = H.random_field(g, 11)
+        rng = np.random.default_rng(4)
+        idx = rng.choice(v.size, 60, replace=False)
+        v[idx[:30]] = 0.0
+        v[idx[30:]] = -0.0
+    else:
+        v = np.zeros(g.counts[0] * g.counts[1])
+    seg = ctx.extract_zero_set_2d(g, v)
+    rseg, rlen = _ref_zero_set(ref, g, v)
+    assert len(seg) == len(rseg)
+    assert_bitwise(seg, rseg, "segments")
+
+
 def test_slice_2d_matches_reference(ctx, port, ref):
     import ctypes as C
 
