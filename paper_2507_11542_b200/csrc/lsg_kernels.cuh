@@ -12,8 +12,9 @@
 //
 // Generic over the grid dimension D (1..6): one thread per node, the
 // cross-shaped stencil read through the read-only data path (neighbouring
-// threads share lines through L1/L2).  Specialised tiled kernels for the
-// benchmark shapes live in lsg_tiled.cuh.
+// threads share lines through L1/L2).  3-D grids take the 2.5-D tiled
+// kernel in lsg_march3.cuh; this one serves D != 3, the gapped boundary-band
+// launches of slabs, and LSG_KERNEL=generic.
 #pragma once
 
 #include "lsg_device.cuh"
