@@ -1,20 +1,24 @@
 // lsg_march3.cuh — 2.5-D tiled fused stage kernel for 3-D grids (sm_100a).
 //
-// Block = a TX x R tile of the (x, y) plane, marching along z through a chunk
-// of planes.  Each thread owns two x-adjacent nodes (x, x+1), so the x-window
-// (2W+2 values) is shared by the pair, and every shared-memory access is a
-// 128-bit load of a node pair.  Per plane:
-//   * the tile and a W-wide halo ring (cross-shaped, no corners) are staged in
-//     shared memory: centre pairs come from the threads' registers, halo slots
-//     are prefetched one plane ahead and already hold the padded-line value
-//     (in-range node, periodic wrap, or the extrapolated ghost
-//     a + k*(a - b), grid.cpp:108-128), so every window is a plain read;
-//   * the z-windows of both nodes live in registers and slide one plane,
-//     the next value prefetched one plane ahead (slab halo planes / global
-//     ghosts resolved at load time, uniformly per block);
+// Block = a TX x R tile of the (x, y) plane (full rows when they fit, else
+// x segments), marching along z through a balanced chunk of planes.  Each
+// thread owns two x-adjacent nodes (x, x+1), so the x-window (2W+2 values) is
+// shared by the pair, and every shared-memory access is a 128-bit load of a
+// node pair.
+//   * Planes stream through a shared-memory ring of 2W+1+D slots (D = 2
+//     planes in flight) filled by cp.async: each thread copies its own pair
+//     and up to kMaxHalo halo slots of a W-wide cross-shaped ring.  Halo
+//     slots hold the padded-line value (in-range node, periodic wrap, or the
+//     extrapolated ghost a + k*(a - b) written by a ghost pass,
+//     grid.cpp:108-128), so every window is a plain read.  Ghost planes
+//     beyond a global z edge are extrapolated at load time; slab halo planes
+//     are read from the buffer.  One barrier per plane.
+//   * The z-window of a pair is the pair's slot in the 2W+1 resident planes.
 //   * L/R per dimension, central costate, H, global-LF dissipation, clamp and
 //     the TVD-RK combination use exactly the arithmetic of stage_kernel, so
 //     results are bit-identical to it and to the reference.
+//   * The stage's v range (step log) is reduced per block (block_range).
+//   * Programmatic dependent launch: set-up runs before griddepcontrol.wait.
 #pragma once
 
 #include "lsg_kernels.cuh"
