@@ -13,6 +13,13 @@
 // enqueues every stage of the leg back to back with no host synchronisation,
 // and synchronises once at the end of the leg to collect the per-step v range
 // (fused into the last stage of each step) and the error flags.
+//
+// Also here: the stream-ordered device pool and the per-context solver cache
+// of the stateless calls; slabs (halo planes, boundary bands on a side
+// stream, the halo exchange on a communication stream overlapped with the
+// interior, NCCL for ranks / device copies in process); and
+// lsg_solver_step_host (host-to-host step, copies chunked along the slab axis
+// and overlapped with the stage kernels).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
