@@ -235,6 +235,11 @@ SolveOutcome solve_brt(const ProblemSetup& setup, std::pair<double, double> tspa
 ScalarField sphere(GridPtr grid, const std::vector<double>& center, double radius);
 ScalarField cylinder(GridPtr grid, const std::set<int>& ignored_dims, const std::vector<double>& center,
                      double radius);
+ScalarField rectangle(GridPtr grid, const std::vector<double>& lower, const std::vector<double>& upper);
+ScalarField ellipsoid(GridPtr grid, double radius);
+ScalarField set_union(const ScalarField& a, const ScalarField& b);
+ScalarField set_intersection(const ScalarField& a, const ScalarField& b);
+ScalarField set_complement(const ScalarField& a);
 
 // ---- runner.hpp: convergence study on the device kernels ---------------------------
 struct ConvergenceRow {

@@ -188,6 +188,9 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
                 const double* v, double* dvdt, double* step_bound);
 /* restrict_update (hamiltonian.hpp:62, hamiltonian.cpp:78-88). */
 int lsg_restrict_update(lsg_ctx* ctx, size_t n, const double* dvdt, int direction, double* out);
+/* set_union / set_intersection / set_complement on host fields (implicit_surfaces.cpp:128-151):
+ * op 1 = std::min(a, b), 2 = std::max(a, b), 3 = -a (b unused). */
+int lsg_set_op(lsg_ctx* ctx, int op, size_t n, const double* a, const double* b, double* out);
 /* integrate / ode_cfl_1/2/3 with the Lax-Friedrichs term
  * (integrator.hpp:49-72, integrator.cpp:22-125).  v is the initial value on
  * entry and the final value on return; steps receives up to log_cap entries
@@ -241,9 +244,19 @@ int lsg_solver_get_field(lsg_solver* s, double* host_v);
 int lsg_solver_set_field_device(lsg_solver* s, const double* dev_v);
 int lsg_solver_field_device(lsg_solver* s, double** dev_v);
 /* Device initial-condition generator (implicit_surfaces.cpp:20-71):
- * shape 0 = sphere(center, radius), 1 = cylinder(ignored_mask, center, radius). */
+ * shape 0 = sphere(center, radius), 1 = cylinder(ignored_mask, center, radius),
+ * 2 = planar pair distance (6-D).  Writes a fresh field. */
 int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const double* center,
                           double radius);
+/* The same generator with every implicit_surfaces.cpp shape, composed with the
+ * resident field on the device: op 0 = replace, 1 = set_union (std::min(field,
+ * shape)), 2 = set_intersection (std::max(field, shape)) (implicit_surfaces.cpp:128-145).
+ * shape 3 = rectangle(lower = center[], upper[]) (:73-94), 4 = ellipsoid(radius),
+ * 2-D/3-D (:96-116); shapes 0-2 as in lsg_solver_init_shape. */
+int lsg_solver_apply_shape(lsg_solver* s, int op, int shape, unsigned ignored_mask, const double* center,
+                           const double* upper, double radius);
+/* field = -field (set_complement, implicit_surfaces.cpp:147-151). */
+int lsg_solver_complement(lsg_solver* s);
 /* CFL step bound 1/sum(alpha_d/dx_d) at time t (hamiltonian.cpp:44-71). */
 int lsg_solver_step_bound(lsg_solver* s, double t, double* bound);
 /* Enqueue one TVD-RK step of size dt from time t (integrator.cpp:58-85) on the

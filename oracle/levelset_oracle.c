@@ -614,3 +614,59 @@ int orc_cylinder(const lsg_grid* g, unsigned ignored_mask, const double* center,
 int orc_sphere(const lsg_grid* g, const double* center, double radius, double* out) {
     return orc_cylinder(g, 0u, center, radius, out);
 }
+
+/* implicit_surfaces.cpp:73-94 */
+int orc_rectangle(const lsg_grid* g, const double* lower, const double* upper, double* out) {
+    int rc = orc_grid_check(g);
+    if (rc) return rc;
+    for (int d = 0; d < g->dim; ++d)
+        if (!(upper[d] > lower[d])) return fail(LSG_EINVAL, "rectangle: upper must exceed lower");
+    const size_t N = orc_node_count(g);
+    double* axes[LSG_MAX_DIM];
+    for (int d = 0; d < g->dim; ++d) {
+        axes[d] = (double*)malloc(sizeof(double) * (size_t)g->counts[d]);
+        orc_axis(g, d, axes[d]);
+    }
+    double x[LSG_MAX_DIM];
+    for (size_t i = 0; i < N; ++i) {
+        coords_of(g, axes, i, x);
+        double v = -INFINITY;
+        for (int d = 0; d < g->dim; ++d) v = smax(v, smax(lower[d] - x[d], x[d] - upper[d]));
+        out[i] = v;
+    }
+    for (int d = 0; d < g->dim; ++d) free(axes[d]);
+    return LSG_OK;
+}
+
+/* implicit_surfaces.cpp:96-116 */
+int orc_ellipsoid(const lsg_grid* g, double radius, double* out) {
+    int rc = orc_grid_check(g);
+    if (rc) return rc;
+    if (g->dim != 2 && g->dim != 3) return fail(LSG_EINVAL, "ellipsoid: only 2-D and 3-D grids are supported");
+    if (!(radius > 0.0)) return fail(LSG_EINVAL, "ellipsoid: radius must be positive");
+    const size_t N = orc_node_count(g);
+    double* axes[LSG_MAX_DIM];
+    for (int d = 0; d < g->dim; ++d) {
+        axes[d] = (double*)malloc(sizeof(double) * (size_t)g->counts[d]);
+        orc_axis(g, d, axes[d]);
+    }
+    double x[LSG_MAX_DIM];
+    for (size_t i = 0; i < N; ++i) {
+        coords_of(g, axes, i, x);
+        double v = x[0] * x[0] + 4.0 * x[1] * x[1];
+        if (g->dim == 3) v += 9.0 * x[2] * x[2];
+        out[i] = v - radius;
+    }
+    for (int d = 0; d < g->dim; ++d) free(axes[d]);
+    return LSG_OK;
+}
+
+/* implicit_surfaces.cpp:128-151: op 1 union (std::min), 2 intersection (std::max), 3 complement */
+int orc_set_op(const lsg_grid* g, int op, const double* a, const double* b, double* out) {
+    int rc = orc_grid_check(g);
+    if (rc) return rc;
+    const size_t N = orc_node_count(g);
+    for (size_t i = 0; i < N; ++i)
+        out[i] = op == 1 ? smin(a[i], b[i]) : (op == 2 ? smax(a[i], b[i]) : -a[i]);
+    return LSG_OK;
+}

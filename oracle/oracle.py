@@ -161,6 +161,26 @@ class _Checker:
         return out
 
 
+    def rectangle(self, g, lower, upper):
+        out = np.empty(_n(g), dtype=np.float64)
+        lo = np.ascontiguousarray(lower, dtype=np.float64)
+        up = np.ascontiguousarray(upper, dtype=np.float64)
+        self._call("rectangle", C.byref(g), abi.dptr(lo), abi.dptr(up), abi.dptr(out))
+        return out
+
+    def ellipsoid(self, g, radius):
+        out = np.empty(_n(g), dtype=np.float64)
+        self._call("ellipsoid", C.byref(g), C.c_double(radius), abi.dptr(out))
+        return out
+
+    def set_op(self, g, op, a, b=None):
+        out = np.empty(_n(g), dtype=np.float64)
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = a if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        self._call("set_op", C.byref(g), C.c_int(op), abi.dptr(a), abi.dptr(b), abi.dptr(out))
+        return out
+
+
 class _Reference(_Checker):
     def solve_rockets(self, n, tspan, n_checkpoints, theta_periodic=False, log_cap=1 << 16):
         N = n ** 3

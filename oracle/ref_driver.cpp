@@ -390,6 +390,37 @@ int ref_cylinder(const lsg_grid* g, unsigned ignored_mask, const double* center,
     });
 }
 
+// implicit_surfaces.cpp:73-151
+int ref_rectangle(const lsg_grid* g, const double* lower, const double* upper, double* out) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        ScalarField f = rectangle(grid, std::vector<double>(lower, lower + grid->dim()),
+                                  std::vector<double>(upper, upper + grid->dim()));
+        std::memcpy(out, f.values().data(), f.size() * sizeof(double));
+    });
+}
+
+int ref_ellipsoid(const lsg_grid* g, double radius, double* out) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        ScalarField f = ellipsoid(grid, radius);
+        std::memcpy(out, f.values().data(), f.size() * sizeof(double));
+    });
+}
+
+// op 1 set_union, 2 set_intersection, 3 set_complement (b unused)
+int ref_set_op(const lsg_grid* g, int op, const double* a, const double* b, double* out) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        const std::size_t n = grid->node_count();
+        ScalarField fa(grid, std::vector<double>(a, a + n));
+        ScalarField r = op == 3 ? set_complement(fa)
+                                : (op == 1 ? set_union(fa, ScalarField(grid, std::vector<double>(b, b + n)))
+                                           : set_intersection(fa, ScalarField(grid, std::vector<double>(b, b + n))));
+        std::memcpy(out, r.values().data(), n * sizeof(double));
+    });
+}
+
 // CPU baseline: `nthreads` concurrent independent replicas of the reference's
 // integrate(method, LF term, {0, tf}, v0, opts) — the bench_kernels.cpp:70-83
 // pattern, timed with steady_clock.  Returns wall seconds and the accepted

@@ -23,12 +23,13 @@ EXPORTS = (
     "lsg_ctx_create", "lsg_nccl_unique_id", "lsg_ctx_create_dist", "lsg_ctx_destroy",
     "lsg_ctx_synchronize", "lsg_ctx_launch_count", "lsg_host_alloc", "lsg_host_free",
     "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis", "lsg_slab_partition",
-    "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update",
+    "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update", "lsg_set_op",
     "lsg_integrate", "lsg_solve_brt", "lsg_write_snapshot", "lsg_read_snapshot",
     "lsg_extract_zero_set_2d", "lsg_slice_2d",
     "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
     "lsg_solver_set_field", "lsg_solver_get_field", "lsg_solver_set_field_device",
-    "lsg_solver_field_device", "lsg_solver_init_shape", "lsg_solver_step_bound", "lsg_solver_step",
+    "lsg_solver_field_device", "lsg_solver_init_shape", "lsg_solver_apply_shape", "lsg_solver_complement",
+    "lsg_solver_step_bound", "lsg_solver_step",
     "lsg_solver_step_host",
     "lsg_solver_step_timed",
     "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
@@ -142,6 +143,14 @@ class Context:
         b = C.c_double()
         call("lsg_term_lf", self.h, C.byref(g), C.byref(p), C.c_double(t), abi.dptr(v), abi.dptr(out), C.byref(b))
         return out, b.value
+
+    def set_op(self, op, a, b=None):
+        """set_union (1) / set_intersection (2) / set_complement (3) of host fields on the device."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = a if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        out = np.empty_like(a)
+        call("lsg_set_op", self.h, C.c_int(op), C.c_size_t(a.size), abi.dptr(a), abi.dptr(b), abi.dptr(out))
+        return out
 
     def restrict_update(self, dvdt, direction):
         dvdt = np.ascontiguousarray(dvdt, dtype=np.float64)
@@ -270,6 +279,23 @@ class Solver:
         c = np.zeros(abi.MAX_DIM, dtype=np.float64)
         c[: len(center)] = center
         call("lsg_solver_init_shape", self.h, C.c_int(shape), C.c_uint(mask), abi.dptr(c), C.c_double(radius))
+
+    def apply_shape(self, op, shape, center=None, radius=1.0, ignored_dims=(), upper=None):
+        """Compose an implicit surface into the resident field on the device
+        (lsg_solver_apply_shape): op 0 replace, 1 union, 2 intersection; shape
+        0 sphere, 1 cylinder, 2 pair distance, 3 rectangle (center = lower
+        corner, upper), 4 ellipsoid (radius)."""
+        D = self.g.dim
+        c = (C.c_double * 6)(*(list(center) if center is not None else [0.0] * D))
+        u = (C.c_double * 6)(*(list(upper) if upper is not None else [0.0] * D))
+        mask = 0
+        for d in ignored_dims:
+            mask |= 1 << d
+        call("lsg_solver_apply_shape", self.h, C.c_int(op), C.c_int(shape), C.c_uint(mask), c, u,
+             C.c_double(radius))
+
+    def complement(self):
+        call("lsg_solver_complement", self.h)
 
     def step_bound(self, t=0.0):
         b = C.c_double()

@@ -99,17 +99,18 @@ std::vector<StepLogEntry> to_steps(const std::vector<lsg_steplog>& log, std::siz
 
 // Device initial condition (lsg_solver_init_shape) on a scratch solver.
 ScalarField device_shape(const GridPtr& grid, int shape, unsigned ignored, const std::vector<double>& center,
-                         double radius) {
+                         double radius, const std::vector<double>& upper = {}) {
     lsg_grid g = to_c(*grid);
     lsg_problem p{};
     p.kind = LSG_HAM_LINEAR;
     p.scheme = LSG_SCHEME_FIRST;
     lsg_solver* s = nullptr;
     check(lsg_solver_create(ctx(), &g, &p, LSG_CFL1, &s));
-    double c[LSG_MAX_DIM] = {0, 0, 0, 0, 0, 0};
+    double c[LSG_MAX_DIM] = {0, 0, 0, 0, 0, 0}, u[LSG_MAX_DIM] = {0, 0, 0, 0, 0, 0};
     for (std::size_t d = 0; d < center.size() && d < LSG_MAX_DIM; ++d) c[d] = center[d];
+    for (std::size_t d = 0; d < upper.size() && d < LSG_MAX_DIM; ++d) u[d] = upper[d];
     ScalarField out(grid);
-    int rc = lsg_solver_init_shape(s, shape, ignored, c, radius);
+    int rc = lsg_solver_apply_shape(s, 0, shape, ignored, c, u, radius);
     if (rc == LSG_OK) rc = lsg_solver_get_field(s, out.values().data());
     lsg_solver_destroy(s);
     check(rc);
@@ -575,5 +576,42 @@ ScalarField cylinder(GridPtr grid, const std::set<int>& ignored_dims, const std:
         throw std::invalid_argument("cylinder: at least one dimension must remain active");
     return device_shape(grid, 1, mask, center, radius);
 }
+
+// implicit_surfaces.cpp:73-151 (argument checks and messages as the reference's)
+ScalarField rectangle(GridPtr grid, const std::vector<double>& lower, const std::vector<double>& upper) {
+    if (!grid) throw std::invalid_argument("rectangle: null grid");
+    const std::size_t dim = static_cast<std::size_t>(grid->dim());
+    if (lower.size() != dim || upper.size() != dim)
+        throw std::invalid_argument("rectangle: corner length must equal the grid dimension");
+    for (std::size_t d = 0; d < dim; ++d)
+        if (!(upper[d] > lower[d]))
+            throw std::invalid_argument("rectangle: upper must exceed lower in dimension " + std::to_string(d));
+    return device_shape(grid, 3, 0u, lower, 0.0, upper);
+}
+
+ScalarField ellipsoid(GridPtr grid, double radius) {
+    if (!grid) throw std::invalid_argument("ellipsoid: null grid");
+    if (grid->dim() != 2 && grid->dim() != 3)
+        throw std::invalid_argument("ellipsoid: only 2-D and 3-D grids are supported");
+    if (!(radius > 0.0)) throw std::invalid_argument("ellipsoid: radius must be positive");
+    return device_shape(grid, 4, 0u, {}, radius);
+}
+
+namespace {
+ScalarField device_set_op(int op, const ScalarField& a, const ScalarField* b, const char* what) {
+    if (b && a.grid_ptr() != b->grid_ptr())
+        throw std::invalid_argument(std::string(what) + ": operands must share a grid");
+    ScalarField out(a.grid_ptr());
+    check(lsg_set_op(ctx(), op, a.size(), a.values().data(), b ? b->values().data() : nullptr,
+                     out.values().data()));
+    return out;
+}
+}  // namespace
+
+ScalarField set_union(const ScalarField& a, const ScalarField& b) { return device_set_op(1, a, &b, "set_union"); }
+ScalarField set_intersection(const ScalarField& a, const ScalarField& b) {
+    return device_set_op(2, a, &b, "set_intersection");
+}
+ScalarField set_complement(const ScalarField& a) { return device_set_op(3, a, nullptr, "set_complement"); }
 
 }  // namespace levelset

@@ -1670,6 +1670,24 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
     });
 }
 
+int lsg_set_op(lsg_ctx* ctx, int op, size_t n, const double* a, const double* b, double* out) {
+    return guarded([&] {
+        activate(ctx);
+        if (op < 1 || op > 3) fail(LSG_EINVAL, "set_op: unknown operation");
+        if (n == 0) return;
+        if (!a || !out || (op != 3 && !b)) fail(LSG_EINVAL, "set_op: null buffer");
+        double* da = ctx->staging(0, sizeof(double) * n);
+        double* db = ctx->staging(1, sizeof(double) * n);
+        double* dout = ctx->staging(2, sizeof(double) * n);
+        CUDA_CHECK(cudaMemcpyAsync(da, a, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (op != 3) CUDA_CHECK(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        launch_set_op(op, static_cast<long long>(n), da, db, dout, ctx->stream);
+        ctx->note_launch();
+        CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int lsg_restrict_update(lsg_ctx* ctx, size_t n, const double* dvdt, int direction, double* out) {
     return guarded([&] {
         activate(ctx);
@@ -1839,12 +1857,15 @@ int lsg_solver_field_device(lsg_solver* s, double** dev_v) {
     });
 }
 
-int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const double* center, double radius) {
+int lsg_solver_apply_shape(lsg_solver* s, int op, int shape, unsigned ignored_mask, const double* center,
+                           const double* upper, double radius) {
     return guarded([&] {
         if (!s) fail(LSG_EINVAL, "null solver");
         activate(s->ctx);
-        if (shape < 0 || shape > 2) fail(LSG_EINVAL, "init_shape: unknown shape");
-        if (!(radius > 0.0)) fail(LSG_EINVAL, "init_shape: radius must be positive");
+        if (op < 0 || op > 2) fail(LSG_EINVAL, "apply_shape: unknown operation");
+        if (shape < 0 || shape > 4) fail(LSG_EINVAL, "init_shape: unknown shape");
+        // implicit_surfaces.cpp argument checks, same messages
+        if (shape <= 2 && !(radius > 0.0)) fail(LSG_EINVAL, "init_shape: radius must be positive");
         if (shape == 2 && s->D != 6) fail(LSG_EINVAL, "init_shape: pair distance needs a 6-D grid");
         if (shape == 1) {
             if (ignored_mask == 0) fail(LSG_EINVAL, "cylinder: ignored_dims must be nonempty");
@@ -1852,7 +1873,17 @@ int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const
             if (__builtin_popcount(ignored_mask) >= s->D)
                 fail(LSG_EINVAL, "cylinder: at least one dimension must remain active");
         }
-        s->cur = 0;
+        if (shape == 3) {
+            if (!center || !upper) fail(LSG_EINVAL, "rectangle: corner length must equal the grid dimension");
+            for (int d = 0; d < s->D; ++d)
+                if (!(upper[d] > center[d]))
+                    fail(LSG_EINVAL, "rectangle: upper must exceed lower in dimension " + std::to_string(d));
+        }
+        if (shape == 4) {
+            if (s->D != 2 && s->D != 3) fail(LSG_EINVAL, "ellipsoid: only 2-D and 3-D grids are supported");
+            if (!(radius > 0.0)) fail(LSG_EINVAL, "ellipsoid: radius must be positive");
+        }
+        if (op == 0) s->cur = 0;  // a fresh field; compositions act on the current one
         invalidate_halos(s);
         for (Slab& sl : s->slabs) {
             ShapeParams S{};
@@ -1862,13 +1893,32 @@ int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const
                 S.n[d] = d == s->D - 1 ? sl.nz : s->g.counts[d];
                 S.axis[d] = s->axis[d];
                 S.center[d] = center ? center[d] : 0.0;
+                S.upper[d] = upper ? upper[d] : 0.0;
             }
             S.z0 = sl.z0;
             S.shape = shape;
-            S.ignored_mask = shape == 0 ? 0u : ignored_mask;
+            S.op = op;
+            S.ignored_mask = shape == 1 ? ignored_mask : 0u;
             S.radius = radius;
-            S.out = sl.f[0];
+            S.out = sl.f[s->cur];
             launch_shape(S, s->ctx->stream);
+            s->ctx->note_launch();
+        }
+    });
+}
+
+int lsg_solver_init_shape(lsg_solver* s, int shape, unsigned ignored_mask, const double* center, double radius) {
+    if (shape > 2) return guarded([&] { fail(LSG_EINVAL, "init_shape: unknown shape"); });
+    return lsg_solver_apply_shape(s, 0, shape, ignored_mask, center, nullptr, radius);
+}
+
+int lsg_solver_complement(lsg_solver* s) {
+    return guarded([&] {
+        if (!s) fail(LSG_EINVAL, "null solver");
+        activate(s->ctx);
+        invalidate_halos(s);
+        for (Slab& sl : s->slabs) {
+            launch_set_op(3, sl.nodes, sl.f[s->cur], sl.f[s->cur], sl.f[s->cur], s->ctx->stream);
             s->ctx->note_launch();
         }
     });

@@ -99,8 +99,14 @@ void launch_restrict(const double* in, double* out, long long n, int direction, 
     restrict_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(in, out, n, direction);
 }
 
-// shape 0 sphere / 1 cylinder (implicit_surfaces.cpp:20-71); 2 planar pair
-// distance |(x0,x1)-(x3,x4)| - r (cfg4 target set, builder-defined).
+// Device initial conditions (implicit_surfaces.cpp:20-126), exact operation
+// order: 0 sphere, 1 cylinder (:20-71), 2 planar pair distance |(x0,x1)-(x3,x4)|
+// - r (cfg4 target set, builder-defined), 3 rectangle (:73-94), 4 ellipsoid
+// (:96-116); composed with the resident field by op (set_union / set_intersection,
+// :128-145: std::min / std::max of (field, shape)).
+__device__ __forceinline__ double std_max(double a, double b) { return (a < b) ? b : a; }  // std::max
+__device__ __forceinline__ double std_min(double a, double b) { return (b < a) ? b : a; }  // std::min
+
 __global__ void __launch_bounds__(256) shape_kernel(const __grid_constant__ ShapeParams S) {
     const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= S.n_local) return;
@@ -117,24 +123,48 @@ __global__ void __launch_bounds__(256) shape_kernel(const __grid_constant__ Shap
         }
         x[d] = S.axis[d][id];
     }
-    double r2 = 0.0;
-    if (S.shape == 2) {
-        const double a = x[0] - x[3];
-        const double b = x[1] - x[4];
-        r2 += a * a;
-        r2 += b * b;
+    double v;
+    if (S.shape == 3) {
+        v = -INFINITY;
+        for (int d = 0; d < S.D; ++d) v = std_max(v, std_max(S.center[d] - x[d], x[d] - S.upper[d]));
+    } else if (S.shape == 4) {
+        v = x[0] * x[0] + 4.0 * x[1] * x[1];
+        if (S.D == 3) v += 9.0 * x[2] * x[2];
+        v = v - S.radius;
     } else {
-        for (int d = 0; d < S.D; ++d) {
-            if (S.ignored_mask & (1u << d)) continue;
-            const double dx = x[d] - S.center[d];
-            r2 += dx * dx;
+        double r2 = 0.0;
+        if (S.shape == 2) {
+            const double a = x[0] - x[3];
+            const double b = x[1] - x[4];
+            r2 += a * a;
+            r2 += b * b;
+        } else {
+            for (int d = 0; d < S.D; ++d) {
+                if (S.ignored_mask & (1u << d)) continue;
+                const double dx = x[d] - S.center[d];
+                r2 += dx * dx;
+            }
         }
+        v = sqrt(r2) - S.radius;
     }
-    S.out[idx] = sqrt(r2) - S.radius;
+    if (S.op == 1) v = std_min(S.out[idx], v);
+    else if (S.op == 2) v = std_max(S.out[idx], v);
+    S.out[idx] = v;
 }
 
 void launch_shape(const ShapeParams& S, cudaStream_t st) {
     shape_kernel<<<(unsigned)((S.n_local + 255) / 256), 256, 0, st>>>(S);
+}
+
+__global__ void __launch_bounds__(256) set_op_kernel(int op, long long n, const double* __restrict__ a,
+                                                     const double* __restrict__ b, double* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = op == 1 ? std_min(a[i], b[i]) : (op == 2 ? std_max(a[i], b[i]) : -a[i]);
+}
+
+void launch_set_op(int op, long long n, const double* a, const double* b, double* out, cudaStream_t st) {
+    set_op_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(op, n, a, b, out);
 }
 
 __global__ void range_init_kernel(unsigned long long* r, long long nslots) {

@@ -14,9 +14,11 @@ struct ShapeParams {
     int n[kMaxDim];
     int z0;
     const double* axis[kMaxDim];
-    int shape;
+    int shape;             // 0 sphere, 1 cylinder, 2 planar pair distance, 3 rectangle, 4 ellipsoid
+    int op;                // 0 replace, 1 union (std::min), 2 intersection (std::max) with out
     unsigned ignored_mask;
-    double center[kMaxDim];
+    double center[kMaxDim];  // sphere/cylinder centre; rectangle lower corner
+    double upper[kMaxDim];   // rectangle upper corner
     double radius;
     double* out;
 };
@@ -54,6 +56,8 @@ void launch_shift(const double* padded, double* out, long long N, int n, long lo
                   cudaStream_t st);
 void launch_restrict(const double* in, double* out, long long n, int direction, cudaStream_t st);
 void launch_shape(const ShapeParams& S, cudaStream_t st);
+// elementwise set operations (implicit_surfaces.cpp:128-151): op 1 min, 2 max, 3 negate a
+void launch_set_op(int op, long long n, const double* a, const double* b, double* out, cudaStream_t st);
 void launch_stamp(unsigned long long* out, cudaStream_t st);  // %globaltimer into *out (tracing)
 void launch_range_init(unsigned long long* r, long long nslots, cudaStream_t st);
 long long zero_set_2d(const double* f, int nx, int ny, const double* ax, const double* ay, double dx, double dy,

@@ -299,8 +299,79 @@ static void contour_tests() {  // contour.cpp via the drop-in
     CHECK_THROWS_AS(extract_zero_set_2d(rk.initial_value), std::invalid_argument);
 }
 
+// test_implicit_surfaces.cpp:66-150 re-expressed against the drop-in
+static void implicit_surface_tests() {
+    auto node = [](const Grid& g, std::initializer_list<int> m) { return g.index(std::vector<int>(m)); };
+    {
+        auto g = Grid::create({-2.0, -2.0}, {2.0, 2.0}, {5, 5});
+        const ScalarField v = rectangle(g, {-1.0, -1.0}, {1.0, 1.0});
+        CHECK(approx(v[node(*g, {2, 2})], -1.0, 1e-14));
+        CHECK(approx(v[node(*g, {4, 2})], 1.0, 1e-14));
+        CHECK(approx(v[node(*g, {3, 3})], 0.0, 1e-14));
+        CHECK(approx(v[node(*g, {4, 4})], 1.0, 1e-14));
+        CHECK_THROWS_AS(rectangle(g, {1.0, -1.0}, {-1.0, 1.0}), std::invalid_argument);
+    }
+    {
+        auto g2 = Grid::create({-3.0, -3.0}, {3.0, 3.0}, {7, 7});
+        const ScalarField e2 = ellipsoid(g2, 4.0);
+        CHECK(approx(e2[node(*g2, {3, 3})], -4.0, 1e-14));
+        CHECK(approx(e2[node(*g2, {3, 4})], 0.0, 1e-14));
+        CHECK(approx(e2[node(*g2, {5, 3})], 0.0, 1e-14));
+        auto g3 = Grid::create({-3.0, -3.0, -3.0}, {3.0, 3.0, 3.0}, {7, 7, 7});
+        const ScalarField e3 = ellipsoid(g3, 9.0);
+        CHECK(approx(e3[node(*g3, {3, 3, 4})], 0.0, 1e-14));
+        CHECK(approx(e3[node(*g3, {6, 3, 3})], 0.0, 1e-14));
+        auto g1 = Grid::create({0.0}, {1.0}, {5});
+        CHECK_THROWS_AS(ellipsoid(g1, 1.0), std::invalid_argument);
+    }
+    {
+        auto g = Grid::create({-2.0, -2.0, -2.0}, {2.0, 2.0, 2.0}, {5, 5, 5});
+        const ScalarField a = sphere(g, {-1.0, 0.0, 0.0}, 1.0);
+        const ScalarField b = sphere(g, {1.0, 0.0, 0.0}, 1.0);
+        const ScalarField u = set_union(a, b);
+        const ScalarField n = set_intersection(a, b);
+        bool ok = true;
+        for (std::size_t i = 0; i < u.size(); ++i)
+            ok = ok && u[i] == std::min(a[i], b[i]) && n[i] == std::max(a[i], b[i]);
+        CHECK(ok);
+        CHECK(approx(u[node(*g, {1, 2, 2})], -1.0, 1e-14));
+        CHECK(approx(u[node(*g, {2, 2, 2})], 0.0, 1e-14));
+        const ScalarField c = set_complement(a);
+        const ScalarField cc = set_complement(c);
+        ok = true;
+        for (std::size_t i = 0; i < c.size(); ++i) ok = ok && c[i] == -a[i] && cc[i] == a[i];
+        CHECK(ok);
+    }
+    {  // De Morgan bit for bit
+        auto g = Grid::create({-2.0, -2.0, -2.0}, {2.0, 2.0, 2.0}, {9, 9, 9});
+        std::mt19937_64 rng(2024);
+        std::uniform_real_distribution<double> center(-1.5, 1.5), radius(0.2, 2.0);
+        bool ok = true;
+        for (int trial = 0; trial < 10; ++trial) {
+            const ScalarField a = sphere(g, {center(rng), center(rng), center(rng)}, radius(rng));
+            const double lo = center(rng);
+            const ScalarField b = rectangle(g, {lo, lo, lo}, {lo + radius(rng), lo + radius(rng), lo + radius(rng)});
+            const ScalarField lhs = set_complement(set_union(a, b));
+            const ScalarField rhs = set_intersection(set_complement(a), set_complement(b));
+            const ScalarField lhs2 = set_complement(set_intersection(a, b));
+            const ScalarField rhs2 = set_union(set_complement(a), set_complement(b));
+            for (std::size_t i = 0; i < lhs.size(); ++i) ok = ok && lhs[i] == rhs[i] && lhs2[i] == rhs2[i];
+        }
+        CHECK(ok);
+    }
+    {
+        auto g1 = Grid::create({-2.0, -2.0, -2.0}, {2.0, 2.0, 2.0}, {5, 5, 5});
+        auto g2 = Grid::create({-2.0, -2.0, -2.0}, {2.0, 2.0, 2.0}, {5, 5, 5});
+        const ScalarField a = sphere(g1, {0.0, 0.0, 0.0}, 1.0);
+        const ScalarField b = sphere(g2, {0.0, 0.0, 0.0}, 1.0);
+        CHECK_THROWS_AS(set_union(a, b), std::invalid_argument);
+        CHECK_THROWS_AS(set_intersection(a, b), std::invalid_argument);
+    }
+}
+
 int main() {
     try {
+        implicit_surface_tests();
         grid_tests();
         derivative_tests();
         hamiltonian_tests();

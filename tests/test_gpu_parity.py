@@ -599,3 +599,48 @@ def test_step_log_signed_zero_extremes(ctx, port, monkeypatch, kernel, counts, n
         assert ta == tb
         assert_bitwise(sa, sb, f"step log {kernel} m={method}")
         assert_bitwise(s.get_field(), vb, f"field {kernel} m={method}")
+
+
+@pytest.mark.parametrize("dims,nslabs", [(2, 1), (3, 1), (3, 3), (4, 1), (4, 2)])
+def test_device_implicit_surface_compositions(ctx, ref, dims, nslabs):
+    """rectangle, ellipsoid and the set operations on the device-resident field
+    (lsg_solver_apply_shape / _complement) against the reference's own
+    implicit_surfaces.cpp functions, bit for bit; the stateless lsg_set_op
+    on host fields likewise."""
+    counts = [21, 17, 15, 9][:dims]
+    g = abi.make_grid([-1.0] * dims, [1.0 + 0.25 * d for d in range(dims)], counts)
+    p = abi.make_problem(abi.HAM_LINEAR, abi.SCHEME_FIRST, abi.linear_params([0.0] * dims), abi.GROW, False)
+    s = _lib.Solver(ctx, g, p, abi.CFL1, nslabs=nslabs)
+    lo, up = [-0.5 + 0.1 * d for d in range(dims)], [0.3 + 0.05 * d for d in range(dims)]
+    c = [0.1 * (d + 1) for d in range(dims)]
+
+    s.apply_shape(0, 3, center=lo, upper=up)
+    want = ref.rectangle(g, lo, up)
+    assert_bitwise(s.get_field(), want, "rectangle")
+    s.apply_shape(1, 0, center=c, radius=0.6)                       # union with a sphere
+    want = ref.set_op(g, 1, want, ref.sphere(g, c, 0.6))
+    assert_bitwise(s.get_field(), want, "rectangle u sphere")
+    if dims in (2, 3):
+        s.apply_shape(2, 4, radius=0.8)                             # intersection with an ellipsoid
+        want = ref.set_op(g, 2, want, ref.ellipsoid(g, 0.8))
+        assert_bitwise(s.get_field(), want, "... n ellipsoid")
+    s.complement()
+    want = ref.set_op(g, 3, want)
+    assert_bitwise(s.get_field(), want, "complement")
+    s.apply_shape(2, 1, center=c, radius=0.4, ignored_dims=(0,))    # intersection with a cylinder
+    want = ref.set_op(g, 2, want, ref.cylinder(g, [0], c, 0.4))
+    assert_bitwise(s.get_field(), want, "... n cylinder")
+    # stateless set operations on host fields
+    b = ref.sphere(g, c, 0.3)
+    for op in (1, 2, 3):
+        assert_bitwise(ctx.set_op(op, want, b), ref.set_op(g, op, want, b), f"lsg_set_op {op}")
+
+
+def test_implicit_surface_argument_errors(ctx):
+    g = abi.make_grid([-1.0] * 4, [1.0] * 4, [7, 7, 7, 7])
+    p = abi.make_problem(abi.HAM_LINEAR, abi.SCHEME_FIRST, abi.linear_params([0.0] * 4), abi.GROW, False)
+    s = _lib.Solver(ctx, g, p, abi.CFL1)
+    with pytest.raises(ValueError, match="ellipsoid: only 2-D and 3-D"):
+        s.apply_shape(0, 4, radius=1.0)
+    with pytest.raises(ValueError, match="rectangle: upper must exceed lower"):
+        s.apply_shape(0, 3, center=[0.0] * 4, upper=[1.0, 1.0, -1.0, 1.0])

@@ -357,3 +357,22 @@ def test_kat_rockets_acceptance_490_steps(port, sums):
     assert len(steps) == e["n_steps"] == 490
     assert [[x.hex() for x in row] for row in steps] == e["steps"]
     assert sha(ck[-1]) == e["out"]
+
+
+@pytest.mark.parametrize("dims", [2, 3, 4])
+def test_port_vs_reference_implicit_surfaces(port, ref, dims):
+    """rectangle / ellipsoid / set_union / set_intersection / set_complement
+    (implicit_surfaces.cpp:73-151): restatement == compiled reference, bit for
+    bit, signed zeros and NaN operands of the set operations included."""
+    g = abi.make_grid([-1.0] * dims, [1.0 + 0.25 * d for d in range(dims)], [9, 8, 7, 6][:dims])
+    lo, up = [-0.5 + 0.1 * d for d in range(dims)], [0.3 + 0.05 * d for d in range(dims)]
+    assert_bitwise(port.rectangle(g, lo, up), ref.rectangle(g, lo, up), "rectangle")
+    if dims in (2, 3):
+        assert_bitwise(port.ellipsoid(g, 0.7), ref.ellipsoid(g, 0.7), "ellipsoid")
+    rng = np.random.default_rng(dims)
+    n = int(np.prod([9, 8, 7, 6][:dims]))
+    a, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    a[:4], b[:4] = [0.0, -0.0, 0.0, np.nan], [-0.0, 0.0, 0.0, 1.0]
+    b[4] = np.nan
+    for op in (1, 2, 3):
+        assert_bitwise(port.set_op(g, op, a, b), ref.set_op(g, op, a, b), f"set op {op}")
