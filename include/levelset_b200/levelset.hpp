@@ -98,6 +98,13 @@ struct PaddedField {
 };
 
 PaddedField pad_ghost(const ScalarField& field, int dim, int width);
+
+namespace detail {
+/// grid.cpp:108-128: one line (n nodes at `base`, step `stride`) into
+/// dst[width..width+n) plus `width` ghost nodes per side (ghost fill on the device).
+void fill_padded_line(std::span<const double> field, std::size_t base, std::size_t stride, int n, int width,
+                      BoundaryCondition bc, std::span<double> dst);
+}  // namespace detail
 ScalarField shift_along_dim(const PaddedField& padded, int offset);
 
 // ---- spatial_derivatives.hpp -----------------------------------------------
@@ -140,8 +147,8 @@ DeviceHamiltonian normal_motion_hamiltonian(double speed = 1.0);
 
 struct HamiltonianProblem {
     GridPtr grid;
-    HamiltonianFn ham_func;              // kept for source compatibility; never called
-    DissipationFn dissipation_bounds;    // kept for source compatibility; never called
+    HamiltonianFn ham_func;              // device kinds: set to the device evaluator (callable like the
+    DissipationFn dissipation_bounds;    // reference's plugins); the solver itself uses `device`, fused
     DerivativeScheme costate_scheme = DerivativeScheme::Eno2;
     UpdateDirection update_direction = UpdateDirection::Grow;
     bool restrict_update = false;
@@ -212,6 +219,10 @@ struct RocketParams {
 };
 
 double rocket_hamiltonian_value(double x, double theta, double p1, double p2, double p3, const RocketParams& params);
+/// reachability.cpp:19-66 on the device (lsg_eval_hamiltonian / lsg_eval_dissipation).
+void rocket_hamiltonian(double t, const Grid& grid, std::span<const ScalarField> costate, ScalarField& out,
+                        const RocketParams& params);
+void rocket_dissipation(double t, const Grid& grid, int dim, ScalarField& out, const RocketParams& params);
 
 struct ProblemSetup {
     HamiltonianProblem problem;

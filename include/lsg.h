@@ -188,6 +188,14 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
                 const double* v, double* dvdt, double* step_bound);
 /* restrict_update (hamiltonian.hpp:62, hamiltonian.cpp:78-88). */
 int lsg_restrict_update(lsg_ctx* ctx, size_t n, const double* dvdt, int direction, double* out);
+/* The reference's Hamiltonian / dissipation plugins (HamiltonianFn / DissipationFn,
+ * hamiltonian.hpp:16-25) for a device kind, on host fields: H at every node from
+ * dim costate fields (costate[d] = central derivative along d), or the per-node
+ * bound on |dH/dp_dim|.  Raw values (term_lax_friedrichs validates them);
+ * e.g. rocket_hamiltonian / rocket_dissipation, reachability.cpp:12-66. */
+int lsg_eval_hamiltonian(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
+                         const double* const* costate, double* out);
+int lsg_eval_dissipation(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t, int dim, double* out);
 /* set_union / set_intersection / set_complement on host fields (implicit_surfaces.cpp:128-151):
  * op 1 = std::min(a, b), 2 = std::max(a, b), 3 = -a (b unused). */
 int lsg_set_op(lsg_ctx* ctx, int op, size_t n, const double* a, const double* b, double* out);

@@ -194,6 +194,16 @@ class _Reference(_Checker):
                          dtype=np.float64).reshape(-1, 5)
         return v, steps
 
+    def rocket_plugins(self, g, params5, costate):
+        """reachability.cpp rocket_hamiltonian / rocket_dissipation on given fields."""
+        n = _n(g)
+        h, b0, b1, b2 = (np.empty(n) for _ in range(4))
+        prm = np.ascontiguousarray(params5, dtype=np.float64)
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in costate]
+        self._call("rocket_plugins", C.byref(g), abi.dptr(prm), abi.dptr(cs[0]), abi.dptr(cs[1]), abi.dptr(cs[2]),
+                   abi.dptr(h), abi.dptr(b0), abi.dptr(b1), abi.dptr(b2))
+        return h, [b0, b1, b2]
+
     def rocket_initial(self, n, theta_periodic=False):
         v = np.empty(n ** 3, dtype=np.float64)
         self._call("rocket_initial", C.c_int(n), C.c_int(1 if theta_periodic else 0), abi.dptr(v))

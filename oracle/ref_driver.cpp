@@ -390,6 +390,32 @@ int ref_cylinder(const lsg_grid* g, unsigned ignored_mask, const double* center,
     });
 }
 
+// reachability.cpp:19-66: the rockets plugins on given costate fields
+int ref_rocket_plugins(const lsg_grid* g, const double* params5, const double* p0, const double* p1,
+                       const double* p2, double* h_out, double* b0, double* b1, double* b2) {
+    return guarded([&] {
+        GridPtr grid = make_grid(g);
+        const std::size_t n = grid->node_count();
+        RocketParams rp;
+        rp.a = params5[0];
+        rp.g = params5[1];
+        rp.capture_radius = params5[2];
+        rp.u_min = params5[3];
+        rp.u_max = params5[4];
+        std::vector<ScalarField> cs;
+        for (const double* c : {p0, p1, p2}) cs.emplace_back(grid, std::vector<double>(c, c + n));
+        ScalarField h(grid);
+        rocket_hamiltonian(0.0, *grid, std::span<const ScalarField>(cs), h, rp);
+        std::memcpy(h_out, h.values().data(), n * sizeof(double));
+        double* bs[3] = {b0, b1, b2};
+        for (int d = 0; d < 3; ++d) {
+            ScalarField b(grid);
+            rocket_dissipation(0.0, *grid, d, b, rp);
+            std::memcpy(bs[d], b.values().data(), n * sizeof(double));
+        }
+    });
+}
+
 // implicit_surfaces.cpp:73-151
 int ref_rectangle(const lsg_grid* g, const double* lower, const double* upper, double* out) {
     return guarded([&] {

@@ -24,6 +24,7 @@ EXPORTS = (
     "lsg_ctx_synchronize", "lsg_ctx_launch_count", "lsg_host_alloc", "lsg_host_free",
     "lsg_grid_check", "lsg_grid_spacing", "lsg_grid_node_count", "lsg_grid_axis", "lsg_slab_partition",
     "lsg_pad_ghost", "lsg_shift_along_dim", "lsg_upwind", "lsg_term_lf", "lsg_restrict_update", "lsg_set_op",
+    "lsg_eval_hamiltonian", "lsg_eval_dissipation",
     "lsg_integrate", "lsg_solve_brt", "lsg_write_snapshot", "lsg_read_snapshot",
     "lsg_extract_zero_set_2d", "lsg_slice_2d",
     "lsg_solver_create", "lsg_solver_create_slabs", "lsg_solver_destroy", "lsg_solver_slab",
@@ -143,6 +144,20 @@ class Context:
         b = C.c_double()
         call("lsg_term_lf", self.h, C.byref(g), C.byref(p), C.c_double(t), abi.dptr(v), abi.dptr(out), C.byref(b))
         return out, b.value
+
+    def eval_hamiltonian(self, g, p, costate, t=0.0):
+        """The device Hamiltonian on host costate fields (HamiltonianFn)."""
+        cs = [np.ascontiguousarray(c, dtype=np.float64) for c in costate]
+        arr = (C.c_void_p * len(cs))(*[c.ctypes.data for c in cs])
+        out = np.empty(node_count(g), dtype=np.float64)
+        call("lsg_eval_hamiltonian", self.h, C.byref(g), C.byref(p), C.c_double(t), arr, abi.dptr(out))
+        return out
+
+    def eval_dissipation(self, g, p, dim, t=0.0):
+        """The device dissipation bound of dimension dim (DissipationFn)."""
+        out = np.empty(node_count(g), dtype=np.float64)
+        call("lsg_eval_dissipation", self.h, C.byref(g), C.byref(p), C.c_double(t), C.c_int(dim), abi.dptr(out))
+        return out
 
     def set_op(self, op, a, b=None):
         """set_union (1) / set_intersection (2) / set_complement (3) of host fields on the device."""

@@ -117,9 +117,57 @@ ScalarField device_shape(const GridPtr& grid, int shape, unsigned ignored, const
     return out;
 }
 
+// The device Hamiltonian / dissipation bound as host-callable plugins (the
+// reference's HamiltonianFn / DissipationFn signatures), for problems built
+// with a device kind.
+void device_eval(const Grid& grid, const DeviceHamiltonian& dev, int dim, std::span<const ScalarField> costate,
+                 ScalarField& out) {
+    lsg_grid g = to_c(grid);
+    lsg_problem p{};
+    p.kind = dev.kind;
+    p.scheme = LSG_SCHEME_FIRST;
+    for (int k = 0; k < LSG_MAX_PARAMS; ++k) p.params[k] = dev.params[static_cast<std::size_t>(k)];
+    if (out.size() != grid.node_count()) throw std::invalid_argument("hamiltonian: output size does not match the grid");
+    if (dim < 0) {
+        std::vector<const double*> cs;
+        for (const ScalarField& c : costate) cs.push_back(c.values().data());
+        check(lsg_eval_hamiltonian(ctx(), &g, &p, 0.0, cs.data(), out.values().data()));
+    } else {
+        check(lsg_eval_dissipation(ctx(), &g, &p, 0.0, dim, out.values().data()));
+    }
+}
+
+void attach_device_plugins(HamiltonianProblem& problem) {
+    const DeviceHamiltonian dev = problem.device;
+    problem.ham_func = [dev](double, const Grid& grid, std::span<const ScalarField> costate, ScalarField& out) {
+        if (costate.size() != static_cast<std::size_t>(grid.dim()))
+            throw std::invalid_argument("hamiltonian: needs one costate field per dimension");
+        device_eval(grid, dev, -1, costate, out);
+    };
+    problem.dissipation_bounds = [dev](double, const Grid& grid, int dim, ScalarField& out) {
+        if (dim < 0 || dim >= grid.dim()) throw std::invalid_argument("dissipation: dimension out of range");
+        device_eval(grid, dev, dim, {}, out);
+    };
+}
+
 }  // namespace
 
 void set_device(int device) { t_device = device; }
+
+namespace detail {
+void fill_padded_line(std::span<const double> field, std::size_t base, std::size_t stride, int n, int width,
+                      BoundaryCondition bc, std::span<double> dst) {
+    std::vector<double> line(static_cast<std::size_t>(n));
+    for (int j = 0; j < n; ++j) line[static_cast<std::size_t>(j)] = field[base + static_cast<std::size_t>(j) * stride];
+    lsg_grid g{};
+    g.dim = 1;
+    g.counts[0] = n;
+    g.mins[0] = 0.0;
+    g.maxs[0] = 1.0;
+    g.periodic_mask = bc == BoundaryCondition::Periodic ? 1u : 0u;
+    check(lsg_pad_ghost(ctx(), &g, line.data(), 0, width, dst.data()));
+}
+}  // namespace detail
 
 // ---- Grid (grid.cpp:9-91) ---------------------------------------------------------
 std::shared_ptr<const Grid> Grid::create(std::vector<double> mins, std::vector<double> maxs, std::vector<int> counts,
@@ -370,6 +418,34 @@ double rocket_hamiltonian_value(double x, double theta, double p1, double p2, do
            params.u_max * std::abs(p1 * x + p3) + params.u_min * std::abs(p2 * x + p3);
 }
 
+namespace {
+DeviceHamiltonian rocket_device(const RocketParams& params) {
+    DeviceHamiltonian d;
+    d.kind = LSG_HAM_ROCKETS;
+    d.params[0] = params.a;
+    d.params[1] = params.g;
+    d.params[2] = params.capture_radius;
+    d.params[3] = params.u_min;
+    d.params[4] = params.u_max;
+    return d;
+}
+}  // namespace
+
+void rocket_hamiltonian(double t, const Grid& grid, std::span<const ScalarField> costate, ScalarField& out,
+                        const RocketParams& params) {
+    (void)t;
+    if (grid.dim() != 3) throw std::invalid_argument("rocket_hamiltonian: grid must be 3-D (x, z, theta)");
+    if (costate.size() != 3) throw std::invalid_argument("rocket_hamiltonian: needs three costate fields");
+    device_eval(grid, rocket_device(params), -1, costate, out);
+}
+
+void rocket_dissipation(double t, const Grid& grid, int dim, ScalarField& out, const RocketParams& params) {
+    (void)t;
+    if (grid.dim() != 3) throw std::invalid_argument("rocket_dissipation: grid must be 3-D (x, z, theta)");
+    if (dim < 0 || dim > 2) throw std::invalid_argument("rocket_dissipation: dimension out of range");
+    device_eval(grid, rocket_device(params), dim, {}, out);
+}
+
 ProblemSetup build_rocket_problem(int points_per_dim, const RocketParams& params, bool theta_periodic) {
     if (points_per_dim < 7) throw std::invalid_argument("build_rocket_problem: needs at least 7 points per dimension");
     if (!(params.u_max > params.u_min)) throw std::invalid_argument("build_rocket_problem: u_max must exceed u_min");
@@ -395,6 +471,7 @@ ProblemSetup build_rocket_problem(int points_per_dim, const RocketParams& params
     problem.device.params[2] = params.capture_radius;
     problem.device.params[3] = params.u_min;
     problem.device.params[4] = params.u_max;
+    attach_device_plugins(problem);
     ScalarField initial = cylinder(grid, {2}, {0.0, 0.0, 0.0}, params.capture_radius);
     return ProblemSetup{std::move(problem), std::move(initial)};
 }
@@ -408,6 +485,7 @@ ProblemSetup rigid_rotation_problem(int points_per_dim) {
     problem.update_direction = UpdateDirection::Grow;
     problem.restrict_update = false;
     problem.device.kind = LSG_HAM_ROTATION;
+    attach_device_plugins(problem);
     ScalarField initial = sphere(grid, {0.5, 0.0}, 0.5);
     return ProblemSetup{std::move(problem), std::move(initial)};
 }

@@ -303,6 +303,19 @@ bool force_generic() {
     return e && std::string(e) == "generic";
 }
 
+EvalFn lookup_eval(int kind, int D) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return eval_lookup_linear(D);
+        case LSG_HAM_NORMAL: return eval_lookup_normal(D);
+        case LSG_HAM_ROTATION: return eval_lookup_rotation(D);
+        case LSG_HAM_ROCKETS: return eval_lookup_rockets(D);
+        case LSG_HAM_AIR3D: return eval_lookup_air3d(D);
+        case LSG_HAM_DBLINT4: return eval_lookup_dblint4(D);
+        case LSG_HAM_DUBINS6: return eval_lookup_dubins6(D);
+    }
+    return nullptr;
+}
+
 AlphaFn lookup_alpha(int kind) {
     switch (kind) {
         case LSG_HAM_LINEAR: return alpha_lookup_linear();
@@ -1667,6 +1680,58 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
         check_alpha_valid(s);
         download(s, dvdt, 1);
         *step_bound = s->bound;
+    });
+}
+
+// The device Hamiltonian (dim < 0) or the dissipation bound of one dimension
+// on host fields: the reference's plugins (HamiltonianFn / DissipationFn,
+// hamiltonian.hpp:16-25) for the device kinds.
+void eval_plugin(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const double* const* costate, int dim,
+                 double* out) {
+    lsg_solver* s = cached_solver(ctx, g, p, LSG_CFL1);
+    CallCache call_cache{ctx};
+    if (s->slabs.size() != 1 || s->distributed) fail(LSG_EINVAL, "plugin evaluation needs a single-rank context");
+    EvalFn fn = lookup_eval(p->kind, g->dim);
+    if (!fn) fail(LSG_EINVAL, "hamiltonian: kind not available for this grid dimension");
+    if (dim >= g->dim) fail(LSG_EINVAL, "dissipation: dimension out of range");
+    const long long N = s->total;
+    EvalParams E{};
+    E.P = slab_params(s, s->slabs[0]);
+    E.dim = dim;
+    if (dim < 0) {
+        double* dc = ctx->staging(0, sizeof(double) * static_cast<size_t>(N * g->dim));
+        for (int d = 0; d < g->dim; ++d) {
+            if (!costate || !costate[d]) fail(LSG_EINVAL, "hamiltonian: costate must hold one field per dimension");
+            CUDA_CHECK(cudaMemcpyAsync(dc + d * N, costate[d], sizeof(double) * N, cudaMemcpyHostToDevice,
+                                       ctx->stream));
+            E.costate[d] = dc + d * N;
+        }
+    }
+    double* dout = ctx->staging(1, sizeof(double) * static_cast<size_t>(N));
+    E.out = dout;
+    void* args[] = {&E};
+    CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(static_cast<unsigned>((N + 255) / 256)),
+                                dim3(256), args, 0, ctx->stream));
+    ctx->note_launch();
+    CUDA_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+}
+
+int lsg_eval_hamiltonian(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
+                         const double* const* costate, double* out) {
+    (void)t;  // every device kind is time-invariant
+    return guarded([&] {
+        if (!out) fail(LSG_EINVAL, "hamiltonian: null output");
+        eval_plugin(ctx, g, p, costate, -1, out);
+    });
+}
+
+int lsg_eval_dissipation(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t, int dim, double* out) {
+    (void)t;
+    return guarded([&] {
+        if (!out) fail(LSG_EINVAL, "dissipation: null output");
+        if (dim < 0) fail(LSG_EINVAL, "dissipation: dimension out of range");
+        eval_plugin(ctx, g, p, nullptr, dim, out);
     });
 }
 

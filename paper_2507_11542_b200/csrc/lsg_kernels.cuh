@@ -198,4 +198,46 @@ __global__ void __launch_bounds__(256) alpha_kernel(const __grid_constant__ Alph
     }
 }
 
+// The device Hamiltonian / dissipation bound as the reference's plugins
+// compute them (HamiltonianFn / DissipationFn, hamiltonian.hpp:16-25): H at
+// every node from D costate fields, or the bound of dimension `dim`; raw
+// values, no validation (term_lax_friedrichs validates).
+struct EvalParams {
+    StageParams P;                  // geometry, coordinate / trig tables, Hamiltonian parameters
+    const double* costate[kMaxDim];
+    int dim;                        // -1: Hamiltonian, else the dissipation bound of this dimension
+    double* out;
+};
+
+template <int KIND, int D>
+__global__ void __launch_bounds__(256) eval_kernel(const __grid_constant__ EvalParams E) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= E.P.n_local) return;
+    int ix[D];
+    double x[kMaxDim] = {0, 0, 0, 0, 0, 0};
+    long long r = idx;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        int i;
+        if (d == D - 1) {
+            i = (int)r;
+        } else {
+            r = divmod_index(r, E.P.n[d], E.P.inv_n[d], i);
+        }
+        ix[d] = (d == D - 1) ? E.P.z0 + i : i;
+        x[d] = __ldg(E.P.axis[d] + ix[d]);
+    }
+    const Trig tr = load_trig<KIND>(E.P, D > 2 ? ix[D > 2 ? 2 : 0] : 0, D > 5 ? ix[D > 5 ? 5 : 0] : 0);
+    if (E.dim < 0) {
+        double p[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) p[d] = __ldg(E.costate[d] + idx);
+        E.out[idx] = hamiltonian<KIND, D>(E.P, x, tr, p);
+    } else {
+        E.out[idx] = dissipation_bound<KIND>(E.P.hp, E.dim, x, tr.c2, tr.s2);
+    }
+}
+
+using EvalFn = void (*)(EvalParams);
+
 }  // namespace lsg

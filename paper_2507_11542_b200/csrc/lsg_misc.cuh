@@ -41,6 +41,13 @@ StageFn stage_lookup_rockets(int D, int s, int m);
 StageFn stage_lookup_air3d(int D, int s, int m);
 StageFn stage_lookup_dblint4(int D, int s, int m);
 StageFn stage_lookup_dubins6(int D, int s, int m);
+EvalFn eval_lookup_linear(int D);
+EvalFn eval_lookup_normal(int D);
+EvalFn eval_lookup_rotation(int D);
+EvalFn eval_lookup_rockets(int D);
+EvalFn eval_lookup_air3d(int D);
+EvalFn eval_lookup_dblint4(int D);
+EvalFn eval_lookup_dubins6(int D);
 AlphaFn alpha_lookup_linear();
 AlphaFn alpha_lookup_normal();
 AlphaFn alpha_lookup_rotation();

@@ -3,6 +3,7 @@
 // layer (include/levelset_b200/levelset.hpp), i.e. reference-style call sites
 // compiled unchanged except for the header and the device Hamiltonian.
 // Run by tests/test_gpu_shim.py on the GPU box; prints one line per failure.
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -369,8 +370,73 @@ static void implicit_surface_tests() {
     }
 }
 
+// reachability.hpp plugins on the device (test_reachability.cpp:115-143 re-expressed
+// for the closed form) and detail::fill_padded_line
+static void plugin_tests() {
+    const RocketParams prm;
+    auto g = Grid::create({-64.0, -64.0, -4.0}, {64.0, 64.0, 4.0}, {9, 9, 9});
+    std::array<ScalarField, 3> bounds = {ScalarField(g), ScalarField(g), ScalarField(g)};
+    for (int d = 0; d < 3; ++d) rocket_dissipation(0.0, *g, d, bounds[static_cast<std::size_t>(d)], prm);
+    std::mt19937_64 rng(47);
+    std::uniform_real_distribution<double> costate(-3.0, 3.0);
+    std::vector<ScalarField> cs = {ScalarField(g), ScalarField(g), ScalarField(g)};
+    for (auto& c : cs)
+        for (std::size_t i = 0; i < c.size(); ++i) c[i] = costate(rng);
+    ScalarField h(g);
+    rocket_hamiltonian(0.0, *g, std::span<const ScalarField>(cs), h, prm);
+    const double eps = 1e-6;
+    bool dominated = true, exact = true;
+    for (std::size_t i = 0; i < g->node_count(); ++i) {
+        const double x = g->coords(0)[i], th = g->coords(2)[i];
+        const double p1 = cs[0][i], p2 = cs[1][i], p3 = cs[2][i];
+        exact = exact && h[i] == rocket_hamiltonian_value(x, th, p1, p2, p3, prm);  // same bits
+        for (int d = 0; d < 3; ++d) {
+            const double q1 = p1 + (d == 0 ? eps : 0.0), q2 = p2 + (d == 1 ? eps : 0.0), q3 = p3 + (d == 2 ? eps : 0.0);
+            const double slope = std::abs(rocket_hamiltonian_value(x, th, q1, q2, q3, prm) -
+                                          rocket_hamiltonian_value(x, th, p1, p2, p3, prm)) / eps;
+            dominated = dominated && slope <= bounds[static_cast<std::size_t>(d)][i] + 1e-6;
+        }
+    }
+    CHECK(exact);
+    CHECK(dominated);
+    CHECK_THROWS_AS(rocket_dissipation(0.0, *g, 3, bounds[0], prm), std::invalid_argument);
+    // the plugins a device problem carries evaluate the same thing
+    const ProblemSetup setup = build_rocket_problem(9);
+    const Grid& rg = *setup.problem.grid;
+    std::vector<ScalarField> rcs = {random_field(setup.problem.grid, 1), random_field(setup.problem.grid, 2),
+                                    random_field(setup.problem.grid, 3)};
+    ScalarField a(setup.problem.grid), b(setup.problem.grid);
+    setup.problem.ham_func(0.0, rg, std::span<const ScalarField>(rcs), a);
+    rocket_hamiltonian(0.0, rg, std::span<const ScalarField>(rcs), b, prm);
+    bool same = true;
+    for (std::size_t i = 0; i < a.size(); ++i) same = same && a[i] == b[i];
+    CHECK(same);
+    setup.problem.dissipation_bounds(0.0, rg, 1, a);
+    rocket_dissipation(0.0, rg, 1, b, prm);
+    same = true;
+    for (std::size_t i = 0; i < a.size(); ++i) same = same && a[i] == b[i];
+    CHECK(same);
+    // detail::fill_padded_line == the matching line of pad_ghost
+    auto g2 = Grid::create({-1.0, -1.0}, {1.0, 1.0}, {11, 7}, {1});
+    const ScalarField f = random_field(g2, 9);
+    for (int dim = 0; dim < 2; ++dim) {
+        const PaddedField pf = pad_ghost(f, dim, 3);
+        const int n = g2->count(dim);
+        const std::size_t stride = dim == 0 ? 1 : 11;
+        std::vector<double> dst(static_cast<std::size_t>(n + 6));
+        detail::fill_padded_line(f.values(), 2 * (dim == 0 ? 11 : 1), stride, n, 3, g2->boundary(dim), dst);
+        bool ok = true;
+        for (int j = 0; j < n + 6; ++j) {
+            const std::size_t base = dim == 0 ? 2 * (n + 6) : 2;
+            ok = ok && dst[static_cast<std::size_t>(j)] == pf.data[base + static_cast<std::size_t>(j) * stride];
+        }
+        CHECK(ok);
+    }
+}
+
 int main() {
     try {
+        plugin_tests();
         implicit_surface_tests();
         grid_tests();
         derivative_tests();

@@ -644,3 +644,17 @@ def test_implicit_surface_argument_errors(ctx):
         s.apply_shape(0, 4, radius=1.0)
     with pytest.raises(ValueError, match="rectangle: upper must exceed lower"):
         s.apply_shape(0, 3, center=[0.0] * 4, upper=[1.0, 1.0, -1.0, 1.0])
+
+
+@pytest.mark.parametrize("theta_periodic", [False, True])
+def test_rocket_plugins_match_reference(ctx, ref, theta_periodic):
+    """lsg_eval_hamiltonian / lsg_eval_dissipation for the rockets kind ==
+    the reference's rocket_hamiltonian / rocket_dissipation
+    (reachability.cpp:19-66) on random costate fields, bit for bit."""
+    S = P.rockets(13, theta_periodic=theta_periodic)
+    rng = np.random.default_rng(8)
+    cs = [rng.uniform(-3, 3, 13 ** 3) for _ in range(3)]
+    h, bounds = ref.rocket_plugins(S.grid, list(S.problem.params)[:5], cs)
+    assert_bitwise(ctx.eval_hamiltonian(S.grid, S.problem, cs), h, "H")
+    for d in range(3):
+        assert_bitwise(ctx.eval_dissipation(S.grid, S.problem, d), bounds[d], f"bound {d}")
