@@ -263,6 +263,8 @@ struct ConvergenceRow {
 /// runner.cpp:298-341 with upwind_derivative on the B200 (profile "sin" or "linear").
 std::vector<ConvergenceRow> convergence_study(DerivativeScheme scheme, int refinements,
                                               const std::string& profile = "sin");
+/// runner.cpp:343-359: the study as CSV text (n,dx,max_error,order).
+std::string format_convergence_table(const std::vector<ConvergenceRow>& rows);
 
 // ---- contour.hpp: zero-level-set extraction on the device ----------------------------
 struct Point2 {

@@ -6,6 +6,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <iomanip>
+#include <sstream>
 #include <numbers>
 #include <stdexcept>
 #include <string>
@@ -532,6 +534,25 @@ SolveOutcome solve_brt(const ProblemSetup& setup, std::pair<double, double> tspa
 }
 
 // ---- runner.cpp:298-341 ---------------------------------------------------------------------
+// runner.cpp:343-359, same stream formatting (host presentation of the device study)
+std::string format_convergence_table(const std::vector<ConvergenceRow>& rows) {
+    std::ostringstream os;
+    os << std::setprecision(12);
+    os << "n,dx,max_error,order\n";
+    for (std::size_t i = 0; i < rows.size(); ++i) {
+        const ConvergenceRow& row = rows[i];
+        os << row.n << "," << row.dx << "," << row.max_error << ",";
+        if (i == 0)
+            os << "";
+        else if (row.exact && rows[i - 1].exact)
+            os << "exact";
+        else
+            os << row.order;
+        os << "\n";
+    }
+    return os.str();
+}
+
 std::vector<ConvergenceRow> convergence_study(DerivativeScheme scheme, int refinements, const std::string& profile) {
     if (refinements < 1) throw std::invalid_argument("convergence_study: refinements must be at least 1");
     if (profile != "sin" && profile != "linear")

@@ -434,8 +434,19 @@ static void plugin_tests() {
     }
 }
 
+static void convergence_table_tests() {  // expected text: the reference's format_convergence_table
+    const std::vector<ConvergenceRow> rows = {{11, 0.2, 0.012345678901234, std::nan(""), false},
+                                              {21, 0.1, 0.0031234, 1.98321, false},
+                                              {41, 0.05, 1e-17, 2.0, true},
+                                              {81, 0.025, 2e-17, 0.5, true}};
+    CHECK(format_convergence_table(rows) ==
+          "n,dx,max_error,order\n11,0.2,0.0123456789012,\n21,0.1,0.0031234,1.98321\n41,0.05,1e-17,2\n"
+          "81,0.025,2e-17,exact\n");
+}
+
 int main() {
     try {
+        convergence_table_tests();
         plugin_tests();
         implicit_surface_tests();
         grid_tests();
