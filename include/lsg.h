@@ -146,6 +146,8 @@ int lsg_ctx_create(int device, lsg_ctx** out);
  * and shared out of band (bench.py uses the torch.distributed store). */
 int lsg_nccl_unique_id(void* out128);
 int lsg_ctx_create_dist(int device, int rank, int nranks, const void* nccl_id128, lsg_ctx** out);
+/* Solvers created on a context must be destroyed before it (their buffers are
+ * released on its stream). */
 int lsg_ctx_destroy(lsg_ctx* ctx);
 int lsg_ctx_synchronize(lsg_ctx* ctx);
 /* Number of device kernels this context has launched so far. */

@@ -7,8 +7,10 @@ library is missing this module raises on load, and every compute call raises
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -81,10 +83,26 @@ def _steps(log, n, cap):
                     dtype=np.float64).reshape(-1, 5)
 
 
+_live_contexts = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all():
+    """Destroy solvers before their contexts while the runtime is intact (the
+    interpreter's teardown order would otherwise be arbitrary)."""
+    for ctx in list(_live_contexts):
+        try:
+            ctx.close()
+        except Exception:
+            pass
+
+
 class Context:
-    """One CUDA device + stream (lsg_ctx)."""
+    """One CUDA device + stream (lsg_ctx).  Closing it closes its solvers first."""
 
     def __init__(self, device=0, rank=0, nranks=1, nccl_id=None):
+        self.h = None
+        self._solvers = weakref.WeakSet()
         h = C.c_void_p()
         if nranks > 1 or nccl_id is not None:
             if nccl_id is None or len(nccl_id) != 128:
@@ -95,9 +113,12 @@ class Context:
             call("lsg_ctx_create", C.c_int(device), C.byref(h))
         self.h = h
         self.device, self.rank, self.nranks = device, rank, nranks
+        _live_contexts.add(self)
 
     def close(self):
         if self.h:
+            for s in list(self._solvers):  # a solver's buffers live on this context's stream
+                s.close()
             load().lsg_ctx_destroy(self.h)
             self.h = None
 
@@ -240,6 +261,7 @@ class Solver:
     """Device-resident value function (lsg_solver): the fast path."""
 
     def __init__(self, ctx: Context, g, p, method, nslabs=1):
+        self.h = None
         self.ctx = ctx
         self.g, self.p, self.method = g, p, method
         h = C.c_void_p()
@@ -252,10 +274,12 @@ class Solver:
         z0, nz, nodes = C.c_int(), C.c_int(), C.c_size_t()
         call("lsg_solver_slab", h, C.byref(z0), C.byref(nz), C.byref(nodes))
         self.z0, self.nz, self.local_nodes = z0.value, nz.value, nodes.value
+        ctx._solvers.add(self)
 
     def close(self):
         if self.h:
-            load().lsg_solver_destroy(self.h)
+            if self.ctx.h:  # a closed context already released its solvers
+                load().lsg_solver_destroy(self.h)
             self.h = None
 
     def __del__(self):
