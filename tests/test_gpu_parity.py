@@ -658,3 +658,50 @@ def test_rocket_plugins_match_reference(ctx, ref, theta_periodic):
     assert_bitwise(ctx.eval_hamiltonian(S.grid, S.problem, cs), h, "H")
     for d in range(3):
         assert_bitwise(ctx.eval_dissipation(S.grid, S.problem, d), bounds[d], f"bound {d}")
+
+
+def test_concurrent_contexts_from_threads(port):
+    """Reentrancy (SPEC: the library is used from several host threads, one
+    context each): four threads run stateless and solver integrations on
+    their own contexts concurrently (ctypes releases the GIL); every result
+    is bit-identical to the oracle's, and errors stay per thread."""
+    import threading
+    cases = [P.CONFIGS[n](**H.small(n)) for n in ("cfg1", "cfg2", "cfg5", "rotation")]
+    want = []
+    for S in cases:
+        v0 = H.initial_value(port, S)
+        want.append((v0, port.integrate(S.grid, S.problem, S.method, 0.0, 0.03, v0)))
+    results, errors = [None] * len(cases), []
+
+    def work(k):
+        try:
+            c = _lib.Context(0)
+            S, (v0, (vb, sb, tb)) = cases[k], want[k]
+            for _ in range(3):
+                va, sa, ta = c.integrate(S.grid, S.problem, S.method, 0.0, 0.03, v0)
+                s = _lib.Solver(c, S.grid, S.problem, S.method)
+                s.set_field(v0)
+                ss, ts = s.integrate(0.0, 0.03)
+                results[k] = (va, sa, ta, s.get_field(), ss, ts)
+                s.close()
+                try:  # an error on this thread reports this thread's message
+                    c.integrate(S.grid, S.problem, S.method, 1.0, 0.0, v0)
+                except ValueError as e:
+                    assert "tspan must not be decreasing" in str(e)
+            c.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k, (v0, (vb, sb, tb)) in enumerate(want):
+        va, sa, ta, vs, ss, ts = results[k]
+        assert ta == tb and ts == tb
+        assert_bitwise(sa, sb, f"steps {k}")
+        assert_bitwise(va, vb, f"v {k}")
+        assert_bitwise(ss, sb, f"solver steps {k}")
+        assert_bitwise(vs, vb, f"solver v {k}")
