@@ -32,7 +32,21 @@ def _grid(nz, periodic_z, abi):
     return abi.make_grid([-1.0, 0.0, 0.0], [1.0, 2.0, float(nz - 1)], [10, 9, nz], periodic)
 
 
-def _worker(rank, world, port, nz, periodic_z, scheme, result_q):
+def _order_key(v):
+    """lsg_device.cuh order_key: monotone u64 key, -0.0 sharing +0.0's key."""
+    b = v.view(np.uint64).copy()
+    b[b == np.uint64(0x8000000000000000)] = np.uint64(0)
+    neg = (b >> np.uint64(63)) == np.uint64(1)
+    return np.where(neg, ~b, b | np.uint64(0x8000000000000000))
+
+
+def _key_to_double(k):
+    k = np.uint64(k)
+    b = (k & np.uint64(0x7FFFFFFFFFFFFFFF)) if (k >> np.uint64(63)) else ~k
+    return np.array([b], dtype=np.uint64).view(np.float64)[0]
+
+
+def _worker(rank, world, port, nz, periodic_z, scheme, zero_speed, result_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import sys
@@ -45,13 +59,19 @@ def _worker(rank, world, port, nz, periodic_z, scheme, result_q):
     port_ = O.port()
     g = _grid(nz, periodic_z, abi)
     W = {0: 1, 1: 2, 2: 3, 3: 3}[scheme]
-    p = abi.make_problem(abi.HAM_LINEAR, scheme, abi.linear_params([0.3, -0.8, 1.1]), abi.GROW, True)
+    speed = [0.0, 0.0, 0.0] if zero_speed else [0.3, -0.8, 1.1]
+    p = abi.make_problem(abi.HAM_LINEAR, scheme, abi.linear_params(speed), abi.GROW, True)
     plane = 10 * 9
     v_full = np.random.default_rng(7).uniform(-1, 1, plane * nz)
+    if zero_speed:  # field >= 0 with +0 and -0 in different slabs: the step log's v_min is a zero
+        v_full = 1.0 + np.abs(v_full)
+        first, later = (-0.0, 0.0) if zero_speed == 1 else (0.0, -0.0)
+        v_full[(nz - 2) * plane + 5] = later  # later in index order (last slab)
+        v_full[1 * plane + 3] = first         # first zero in index order (first slab)
     z0, nzl = _lib.slab_partition(nz, world, rank)
     v = v_full[z0 * plane:(z0 + nzl) * plane].copy()
     _, bound = port_.term_lf(g, p, 0.0, v_full)
-    dt = 0.32 * bound
+    dt = 0.32 * bound if np.isfinite(bound) else 0.01
 
     lo = rank - 1 if rank > 0 else (world - 1 if periodic_z else -1)
     hi = rank + 1 if rank < world - 1 else (0 if periodic_z else -1)
@@ -101,8 +121,28 @@ def _worker(rank, world, port, nz, periodic_z, scheme, result_q):
     d3 = stage_term(vh)
     vn = v + (2.0 / 3.0) * ((vh + dt * d3) - v)
 
-    rng = torch.tensor([vn.min(), -vn.max()], dtype=torch.float64)
-    dist.all_reduce(rng, op=dist.ReduceOp.MIN)
+    # the product's per-step range slot: {~min key, max key, ~first zero code},
+    # every word max-reduced across ranks as unsigned 64-bit (lsg_kernels.cuh
+    # block_range, lsg_host.cu run_leg), then decoded like the host
+    def reduced_range(u):
+        keys = _order_key(u)
+        zeros = np.flatnonzero(u == 0.0)
+        gidx = (z0 * plane + zeros).astype(np.uint64)
+        codes = (gidx << np.uint64(1)) | (u[zeros].view(np.uint64) >> np.uint64(63))
+        fz = codes.min() if codes.size else np.uint64(0xFFFFFFFFFFFFFFFF)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, [int(~keys.min()), int(keys.max()), int(~np.uint64(fz))])
+        w = [max(gw[i] for gw in gathered) for i in range(3)]
+        lo, hi = _key_to_double(~np.uint64(w[0])), _key_to_double(w[1])
+        code = int(~np.uint64(w[2]))
+        if code != 0xFFFFFFFFFFFFFFFF:
+            zero = -0.0 if code & 1 else 0.0
+            lo = zero if lo == 0.0 else lo
+            hi = zero if hi == 0.0 else hi
+        return lo, hi
+
+    vmin, vmax = reduced_range(vn)
+    v0min, v0max = reduced_range(v)  # the initial field keeps its signed zeros
     sizes = [None] * world
     dist.all_gather_object(sizes, (z0, vn))
     if rank == 0:
@@ -111,27 +151,39 @@ def _worker(rank, world, port, nz, periodic_z, scheme, result_q):
             full[zz * plane: zz * plane + part.size] = part
         ref_v, ref_steps, _ = port_.integrate(g, p, abi.CFL3, 0.0, dt, v_full, abi.make_opts(max_step=dt))
         same = bool(np.array_equal(full.view(np.int64), ref_v.view(np.int64)))
-        rng_ok = (rng[0].item() == ref_steps[0, 3]) and (-rng[1].item() == ref_steps[0, 4])
-        result_q.put((same, rng_ok, len(ref_steps)))
+        bits = lambda x: np.array([x], dtype=np.float64).view(np.int64)[0]  # noqa: E731
+        rng_ok = bits(vmin) == bits(ref_steps[0, 3]) and bits(vmax) == bits(ref_steps[0, 4])
+        # integrator.cpp:87-90 over the initial field: sequential std::min/max
+        smin = smax = v_full[0]
+        for x in v_full[1:]:
+            smin = x if x < smin else smin
+            smax = x if smax < x else smax
+        rng_ok = rng_ok and bits(v0min) == bits(smin) and bits(v0max) == bits(smax)
+        expect = {0: None, 1: -0.0, 2: 0.0}[zero_speed]
+        zero_ok = expect is None or bits(v0min) == bits(expect)
+        result_q.put((same, rng_ok, len(ref_steps), zero_ok))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,nz,periodic_z,scheme", [
-    (2, 17, False, 2),   # ENO3, extrapolated ends
-    (2, 16, True, 2),    # ENO3, periodic ring of two: both neighbours are the same rank
-    (3, 20, True, 3),    # WENO5 ring of three, uneven slabs 7/7/6
-    (3, 11, False, 1),   # ENO2, thin slabs 4/4/3
+@pytest.mark.parametrize("world,nz,periodic_z,scheme,zero_speed", [
+    (2, 17, False, 2, 0),       # ENO3, extrapolated ends
+    (2, 16, True, 2, 0),        # ENO3, periodic ring of two: both neighbours are the same rank
+    (3, 20, True, 3, 0),        # WENO5 ring of three, uneven slabs 7/7/6
+    (3, 11, False, 1, 0),       # ENO2, thin slabs 4/4/3
+    (3, 12, True, 2, 1),        # -0 first, +0 in a later slab: the first zero's sign wins across ranks
+    (3, 12, True, 2, 2),        # +0 first, -0 later
 ])
-def test_slab_decomposition_gloo(world, nz, periodic_z, scheme):
+def test_slab_decomposition_gloo(world, nz, periodic_z, scheme, zero_speed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.start_processes(_worker, args=(world, _free_port(), nz, periodic_z, scheme, q), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), nz, periodic_z, scheme, zero_speed, q), nprocs=world,
                        join=True, start_method="spawn")
-    same, rng_ok, nsteps = q.get(timeout=60)
+    same, rng_ok, nsteps, zero_ok = q.get(timeout=60)
     assert nsteps == 1
     assert same, "slab-decomposed RK3 step differs from the single-domain oracle"
-    assert rng_ok, "all-reduced v range differs from the oracle's step log"
+    assert rng_ok, "reduced v range (product's word scheme) differs from the oracle's step log"
+    assert zero_ok, "the first zero's sign did not decide v_min across ranks"
 
 
 def test_partition_rule():
