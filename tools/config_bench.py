@@ -14,6 +14,8 @@ RUNS = {
     "cfg5": (P.cfg5_normal, {}, [None, abi.OPT_WENO5_FAST]),
     "cfg5eno3": (P.cfg5_normal, {"scheme": abi.SCHEME_ENO3}, [None]),
     "cfg4": (P.cfg4_dubins6, {}, [abi.OPT_WENO5_FAST, None]),
+    "cfg4eno3": (P.cfg4_dubins6, {"scheme": abi.SCHEME_ENO3}, [None]),
+    "cfg1eno2": (P.cfg1_circle, {}, [None]),
 }
 ctx = _lib.Context(0)
 names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg5", "cfg5eno3"]
