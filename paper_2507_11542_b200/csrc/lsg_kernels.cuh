@@ -23,39 +23,39 @@ namespace lsg {
 
 using StageFn = void (*)(StageParams);
 
+// Warp maximum of a 64-bit key: two 32-bit redux.sync (the maximum's high
+// word, then the largest low word among the lanes holding it).  Every lane
+// of the warp must call it.
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+    const unsigned hi = static_cast<unsigned>(x >> 32), lo = static_cast<unsigned>(x);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    return (static_cast<unsigned long long>(mhi) << 32) | mlo;
+}
+
 // Block reduction of a step's range candidates into its slot:
 // {~min key, max key, ~first zero code} (all max-reduced, also across ranks).
+// Every thread of the block must call it.
 __device__ __forceinline__ void block_range(unsigned long long* slot, unsigned long long kmin, unsigned long long kmax,
                                             unsigned long long fz) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-        fz = min(fz, __shfl_xor_sync(0xffffffffu, fz, off));
-    }
+    unsigned long long nmin = warp_max_u64(~kmin), mx = warp_max_u64(kmax), nfz = warp_max_u64(~fz);
     __shared__ unsigned long long smin[32], smax[32], sfz[32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
-        smin[warp] = kmin;
-        smax[warp] = kmax;
-        sfz[warp] = fz;
+        smin[warp] = nmin;
+        smax[warp] = mx;
+        sfz[warp] = nfz;
     }
     __syncthreads();
     if (warp == 0) {
         const int nw = blockDim.x >> 5;
-        kmin = lane < nw ? smin[lane] : ~0ull;
-        kmax = lane < nw ? smax[lane] : 0ull;
-        fz = lane < nw ? sfz[lane] : ~0ull;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
-            fz = min(fz, __shfl_xor_sync(0xffffffffu, fz, off));
-        }
+        nmin = warp_max_u64(lane < nw ? smin[lane] : 0ull);
+        mx = warp_max_u64(lane < nw ? smax[lane] : 0ull);
+        nfz = warp_max_u64(lane < nw ? sfz[lane] : 0ull);
         if (lane == 0) {
-            if (kmin != ~0ull) atomicMax(slot, ~kmin);
-            if (kmax != 0ull) atomicMax(slot + 1, kmax);
-            if (fz != ~0ull) atomicMax(slot + 2, ~fz);
+            if (nmin) atomicMax(slot, nmin);
+            if (mx) atomicMax(slot + 1, mx);
+            if (nfz) atomicMax(slot + 2, nfz);
         }
     }
 }
