@@ -837,6 +837,12 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
     for (int d = 0; d < D; ++d) {
         P.n[d] = d == D - 1 ? sl.nz : s->g.counts[d];
         P.inv_n[d] = 1.0 / P.n[d];
+        if (P.n[d] >= 2) {
+            int l = 0;
+            while ((1LL << l) < P.n[d]) ++l;
+            P.magic[d] = static_cast<unsigned>(((1ULL << (31 + l)) + P.n[d] - 1) / static_cast<unsigned long long>(P.n[d]));
+            P.mshift[d] = l - 1;
+        }
         P.stride[d] = st;
         st *= P.n[d];
         P.bc[d] = bc_of(&s->g, d);
@@ -845,6 +851,11 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
         P.axis[d] = s->axis[d];
         P.tcos[d] = s->tcos[d];
         P.tsin[d] = s->tsin[d];
+    }
+    bool all2 = true;
+    for (int d = 0; d < D - 1; ++d) all2 = all2 && P.n[d] >= 2;
+    if (all2) {  // divmod31 where the dividends fit 31 bits (lsg_device.cuh)
+        P.div31 = (sl.nodes <= (1LL << 31) ? 1 : 0) | ((sl.nodes - 1) / P.n[0] < (1LL << 31) ? 2 : 0);
     }
     P.z0 = sl.z0;
     P.nz_glob = s->g.counts[D - 1];

@@ -75,7 +75,10 @@ __device__ __forceinline__ double stage_node(const StageParams& P, const double*
         if (d == D - 1) {
             i[d] = (int)r;
         } else {
-            r = divmod_index(r, P.n[d], P.inv_n[d], i[d]);
+            if (P.div31 & (d == 0 ? 1 : 2))
+                r = divmod31(static_cast<unsigned>(r), P.n[d], P.magic[d], P.mshift[d], i[d]);
+            else
+                r = divmod_index(r, P.n[d], P.inv_n[d], i[d]);
         }
         ix[d] = (d == D - 1) ? P.z0 + i[d] : i[d];
         x[d] = __ldg(P.axis[d] + ix[d]);
