@@ -396,6 +396,7 @@ struct lsg_solver {
     int m3_threads = 0;
     int m3_pitch = 0;
     int m3_per_sm = 1;
+    int div31_mask = 3;  // LSG_DIV31: which divmod31 paths slab_params may enable (tests)
     size_t m3_smem = 0;
     std::string invalid;  // deferred invalid_argument (raised at the first term evaluation)
     int cur = 0;
@@ -449,6 +450,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->D = g->dim;
     s->W = ghost_width(p->scheme);
     s->distributed = ctx->nranks > 1 || ctx->dist_selftest;
+    if (const char* e = std::getenv("LSG_DIV31")) s->div31_mask = std::atoi(e) & 3;
     s->P = s->distributed ? ctx->nranks : nslabs;
     s->total = node_count(g);
     for (int d = 0; d + 1 < s->D; ++d) s->plane *= g->counts[d];
@@ -656,7 +658,7 @@ std::string solver_key(const lsg_grid* g, const lsg_problem* p, int method) {
     put(&p->options, sizeof p->options);
     put(p->params, sizeof p->params);
     put(&method, sizeof method);
-    for (const char* e : {"LSG_KERNEL", "LSG_M3_R", "LSG_M3_CHUNK"}) {
+    for (const char* e : {"LSG_KERNEL", "LSG_M3_R", "LSG_M3_CHUNK", "LSG_DIV31"}) {
         const char* v = std::getenv(e);
         k += '|';
         if (v) k += v;
@@ -855,7 +857,7 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
     bool all2 = true;
     for (int d = 0; d < D - 1; ++d) all2 = all2 && P.n[d] >= 2;
     if (all2) {  // divmod31 where the dividends fit 31 bits (lsg_device.cuh)
-        P.div31 = (sl.nodes <= (1LL << 31) ? 1 : 0) | ((sl.nodes - 1) / P.n[0] < (1LL << 31) ? 2 : 0);
+        P.div31 = ((sl.nodes <= (1LL << 31) ? 1 : 0) | ((sl.nodes - 1) / P.n[0] < (1LL << 31) ? 2 : 0)) & s->div31_mask;
     }
     P.z0 = sl.z0;
     P.nz_glob = s->g.counts[D - 1];

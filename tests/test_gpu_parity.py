@@ -705,3 +705,30 @@ def test_concurrent_contexts_from_threads(port):
         assert_bitwise(va, vb, f"v {k}")
         assert_bitwise(ss, sb, f"solver steps {k}")
         assert_bitwise(vs, vb, f"solver v {k}")
+
+
+def test_index_division_paths_bitwise(ctx, monkeypatch):
+    """The generic kernel decomposes node indices with the 31-bit multiplier
+    division (divmod31) where the dividends fit 31 bits, and with the 64-bit
+    double-reciprocal division otherwise (slabs of more than 2^31 nodes take
+    it for the first axis only).  LSG_DIV31 forces each combination: all three
+    give the same fields bit for bit (6-D ENO3 and WENO5, 4-D WENO5, 1 and 3 slabs)."""
+    cases = {
+        "cfg4_eno3": (P.cfg4_dubins6(13, scheme=abi.SCHEME_ENO3), 1),
+        "cfg4_weno5": (P.cfg4_dubins6(11), 3),
+        "cfg3": (P.cfg3_dblint4(25), 1),
+    }
+    out = {}
+    for mask in ("0", "2", "3"):
+        monkeypatch.setenv("LSG_DIV31", mask)
+        for name, (S, nslabs) in cases.items():
+            s = _lib.Solver(ctx, S.grid, S.problem, S.method, nslabs=nslabs)
+            s.init_shape(*S.ic[:3], S.ic[3])
+            dt = 0.32 * s.step_bound()
+            s.step(0.0, dt)
+            s.step(dt, dt)
+            out[mask, name] = s.get_field()
+            s.close()
+    for name in cases:
+        assert_bitwise(out["0", name], out["3", name], f"{name}: 64-bit vs 31-bit division")
+        assert_bitwise(out["2", name], out["3", name], f"{name}: mixed vs 31-bit division")
