@@ -356,6 +356,7 @@ def b200_arm(args):
     leg_value = nodes_total * stages * nst.value / leg_s
 
     if rank != 0:
+        dist.destroy_process_group()
         return 0
 
     cpu_value, cpu_info = (None, None)

@@ -143,7 +143,14 @@ int lsg_device_count(int* count);
 int lsg_ctx_create(int device, lsg_ctx** out);
 /* Distributed context: one process per GPU, slabs along the last grid axis.
  * nccl_id is the 128-byte ncclUniqueId rank 0 produced with lsg_nccl_unique_id
- * and shared out of band (bench.py uses the torch.distributed store). */
+ * and shared out of band (bench.py uses the torch.distributed store).  On such
+ * a context the solver-backed calls (lsg_solver_*, lsg_integrate,
+ * lsg_solve_brt, lsg_term_lf) take and return this rank's slab
+ * (lsg_slab_partition; solve_brt's checkpoints are slabs too), grids stay
+ * global, and all ranks must make the same calls in the same order (halo
+ * exchanges and all-reduces inside).  The other stateless calls (lsg_upwind,
+ * lsg_pad_ghost, shapes, set operations, evaluations) work per process on
+ * the whole grid they are given. */
 int lsg_nccl_unique_id(void* out128);
 int lsg_ctx_create_dist(int device, int rank, int nranks, const void* nccl_id128, lsg_ctx** out);
 /* Solvers created on a context must be destroyed before it (their buffers are

@@ -1806,7 +1806,12 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
         // reachability.cpp:138-143
         if (n_checkpoints < 1) fail(LSG_EINVAL, "solve_brt: need at least one checkpoint");
         if (!std::isfinite(t_first) || !std::isfinite(t_second)) fail(LSG_EINVAL, "solve_brt: tspan must be finite");
-        const long long N = node_count(g);
+        long long N = node_count(g);
+        if (ctx->nranks > 1) {  // distributed context: v0 and the checkpoints are this rank's slab
+            int z0 = 0, nz = 0;
+            partition(g->counts[g->dim - 1], ctx->nranks, ctx->rank, &z0, &nz);
+            N = N / g->counts[g->dim - 1] * nz;
+        }
         const double duration = std::abs(t_second - t_first);
         std::memcpy(checkpoints, v0, sizeof(double) * N);
         checkpoint_times[0] = 0.0;
