@@ -732,3 +732,26 @@ def test_index_division_paths_bitwise(ctx, monkeypatch):
     for name in cases:
         assert_bitwise(out["0", name], out["3", name], f"{name}: 64-bit vs 31-bit division")
         assert_bitwise(out["2", name], out["3", name], f"{name}: mixed vs 31-bit division")
+
+
+def test_cfg4_full_size_slabs_step_log(ctx):
+    """BASELINE configs[3] at full size: 41^6 = 4.75 G nodes (38 GB per field),
+    exact WENO5, with RK2 so both decompositions fit in HBM one after the other
+    (76 GB for one slab, 109 GB for three with their halo planes).  One slab
+    (node indices above 2^31: 64-bit first-axis division) and three slabs
+    (31-bit division, NCCL-free device halo copies) give bit-identical step logs
+    over two steps: every entry holds the exact min and max of all 4.75 G values
+    and the dt, so a single differing node would show."""
+    S = P.cfg4_dubins6(41)
+    out = []
+    for nslabs in (1, 3):
+        s = _lib.Solver(ctx, S.grid, S.problem, abi.CFL2, nslabs=nslabs)
+        s.init_shape(*S.ic[:3], S.ic[3])
+        tf = 2 * 0.32 * s.step_bound()
+        log, t = s.integrate(0.0, tf)
+        out.append((np.asarray(log, dtype=np.float64), t))
+        s.close()
+    assert len(out[0][0]) >= 2
+    assert_bitwise(out[0][0], out[1][0], "step log at 41^6, 1 vs 3 slabs")
+    assert out[0][1] == out[1][1]
+    assert np.all(np.isfinite(out[0][0]))
