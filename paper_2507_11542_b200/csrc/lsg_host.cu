@@ -404,6 +404,7 @@ struct lsg_solver {
     // (set by the exchange that follows each stage's boundary bands; cleared
     // whenever the field is written from outside a stage)
     bool halo_ok[3] = {false, false, false};
+    bool pdl = true;  // programmatic dependent launch between stages (LSG_PDL=0 disables; read at creation)
     cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
     cudaStream_t side = nullptr;  // boundary bands, concurrent with the interior (slabs only)
     cudaStream_t cin = nullptr, cout = nullptr;  // lsg_solver_step_host copy streams (created on first use)
@@ -450,6 +451,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->D = g->dim;
     s->W = ghost_width(p->scheme);
     s->distributed = ctx->nranks > 1 || ctx->dist_selftest;
+    s->pdl = pdl_enabled();
     if (const char* e = std::getenv("LSG_DIV31")) s->div31_mask = std::atoi(e) & 3;
     s->P = s->distributed ? ctx->nranks : nslabs;
     s->total = node_count(g);
@@ -658,7 +660,7 @@ std::string solver_key(const lsg_grid* g, const lsg_problem* p, int method) {
     put(&p->options, sizeof p->options);
     put(p->params, sizeof p->params);
     put(&method, sizeof method);
-    for (const char* e : {"LSG_KERNEL", "LSG_M3_R", "LSG_M3_CHUNK", "LSG_DIV31"}) {
+    for (const char* e : {"LSG_KERNEL", "LSG_M3_R", "LSG_M3_CHUNK", "LSG_DIV31", "LSG_PDL"}) {
         const char* v = std::getenv(e);
         k += '|';
         if (v) k += v;
@@ -910,7 +912,7 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL with the previous stage
-        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        attr[0].val.programmaticStreamSerializationAllowed = s->pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), args));
@@ -923,7 +925,7 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        attr[0].val.programmaticStreamSerializationAllowed = s->pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->fn[mode]), args));
