@@ -506,7 +506,20 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         // per thread wins (full rows of more than ~120 nodes leave too few
         // rows per tile for the halo budget)
         std::vector<std::pair<int, int>> shapes;
-        if (n0 <= 256) shapes.emplace_back((n0 + 1) & ~1, std::max(1, 256 / (((n0 + 1) & ~1) / 2)));
+        if (n0 <= 256) {
+            // where full rows fit, rows split in three even segments when they are
+            // >= 32 wide and need no more tiles: fewer halo rows per node (101^3:
+            // 34x15 instead of 102x5, 1.65 instead of 2.2 loaded values per
+            // node, +2.8 % on the bench)
+            const int tf = (n0 + 1) & ~1, rf = std::max(1, 256 / (tf / 2));
+            const int t3 = (((n0 + 2) / 3) + 1) & ~1, r3 = std::max(1, 256 / (t3 / 2));
+            const long long tiles_f = static_cast<long long>((n1 + rf - 1) / rf);
+            const long long tiles_3 = static_cast<long long>((n0 + t3 - 1) / t3) * ((n1 + r3 - 1) / r3);
+            const int thf = ((tf / 2 * std::min(rf, n1) + 31) / 32) * 32;
+            const bool full_fits = 2 * W * std::min(tf, n0) + 2 * W * std::min(rf, n1) <= kMaxHalo * thf;
+            if (full_fits && t3 >= 32 && tiles_3 <= tiles_f) shapes.emplace_back(t3, r3);
+            shapes.emplace_back(tf, rf);
+        }
         shapes.emplace_back(32, 16);
         shapes.emplace_back(64, 8);
         if (const char* e = std::getenv("LSG_M3_TX")) {  // tuning override
