@@ -78,12 +78,13 @@ def test_fuzz_integrate_bitwise(ctx, port, case):
 
 @st.composite
 def cases3(draw):
-    """3-D cases sized for the tiled kernel's edge cases: full-row tiles
-    (n0 <= 256) and 32-column segment tiles, ragged last tiles, thin z."""
+    """3-D cases sized for the tiled kernel's edge cases: full-row tiles,
+    rows split in three segments (n0 ~ 96-130), searched segment widths
+    (n0 > 256 or rows that do not fit), ragged last tiles, thin z."""
     scheme = draw(st.integers(0, 3))
     lo = MIN_NODES[scheme]
-    n0 = draw(st.one_of(st.integers(lo, 40), st.integers(250, 300)))
-    n1 = draw(st.integers(lo, 40 if n0 <= 40 else 12))
+    n0 = draw(st.one_of(st.integers(lo, 40), st.integers(90, 130), st.integers(250, 300)))
+    n1 = draw(st.integers(lo, 40 if n0 <= 130 else 12))
     n2 = draw(st.integers(lo, 24))
     periodic = [d for d in range(3) if draw(st.booleans())]
     kind = draw(st.sampled_from([abi.HAM_LINEAR, abi.HAM_NORMAL, abi.HAM_AIR3D]))
