@@ -16,7 +16,16 @@ RUNS = {
     "cfg4": (P.cfg4_dubins6, {}, [abi.OPT_WENO5_FAST, None]),
     "cfg4eno3": (P.cfg4_dubins6, {"scheme": abi.SCHEME_ENO3}, [None]),
     "cfg1eno2": (P.cfg1_circle, {}, [None]),
+    # low-arithmetic schemes on the cfg5 grid: how close the tiled kernel's data
+    # movement gets to the HBM roofline when FP64 is not the limit
+    "cfg5first": (P.cfg5_normal, {"scheme": abi.SCHEME_FIRST}, [None]),
+    "cfg5eno2": (P.cfg5_normal, {"scheme": abi.SCHEME_ENO2}, [None]),
 }
+try:
+    HBM_PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                 "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    HBM_PEAK = 6546.2
 ctx = _lib.Context(0)
 names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg5", "cfg5eno3"]
 out = []
@@ -44,6 +53,8 @@ for name in names:
                "stages": len(ms), "stage_ms": [round(float(x), 4) for x in ms],
                "G_node_stage_per_s": round(rate / 1e9, 2),
                "hbm_frac_of_6546": round(rate * (64 / 3 if len(ms) == 3 else 20.0) / 6546.2e9, 4),
+               "hbm_gbs": round(rate * (64 / 3 if len(ms) == 3 else 20.0) / 1e9, 1),
+               "hbm_frac_measured_peak": round(rate * (64 / 3 if len(ms) == 3 else 20.0) / (HBM_PEAK * 1e9), 4),
                "wall_s": round(time.time() - t0, 1)}
         print(json.dumps(rec), flush=True)
         out.append(rec)

@@ -13,8 +13,10 @@ name = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else None
 fast = len(sys.argv) > 3 and sys.argv[3] == "fast"
 build = {"cfg1": P.cfg1_circle, "cfg2": P.cfg2_air3d, "cfg3": P.cfg3_dblint4, "cfg4": P.cfg4_dubins6,
-         "cfg5": P.cfg5_normal, "cfg5eno3": lambda n: P.cfg5_normal(n, scheme=abi.SCHEME_ENO3)}[name]
-S = build(n) if n else build()
+         "cfg5": P.cfg5_normal, "cfg5eno3": lambda n: P.cfg5_normal(n, scheme=abi.SCHEME_ENO3),
+         "cfg5first": lambda n: P.cfg5_normal(n, scheme=abi.SCHEME_FIRST),
+         "cfg5eno2": lambda n: P.cfg5_normal(n, scheme=abi.SCHEME_ENO2)}[name]
+S = build(n) if n else (build() if name in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5") else build(512))
 prob = S.problem
 if fast:
     prob = abi.make_problem(prob.kind, prob.scheme, list(prob.params), prob.direction, bool(prob.restrict_update),
