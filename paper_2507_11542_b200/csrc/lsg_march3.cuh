@@ -96,7 +96,7 @@ struct RingShape {
 
 // Resident blocks per SM: 3 for the narrow First/ENO2 stencils (80 registers,
 // issue-bound at 512^3: +6-7 % over 2), 2 for ENO3/WENO5 (128 registers; 1 and
-// 3 were measured slower, DESIGN.md §9).
+// 3 were measured slower, DESIGN.md §5 and §9).
 template <int S, int KIND, int MODE, bool RANGE>
 __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2) march3_kernel(const __grid_constant__ StageParams P,
                                                                        const __grid_constant__ March3 M) {
