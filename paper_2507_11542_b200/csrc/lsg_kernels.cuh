@@ -110,7 +110,7 @@ __device__ __forceinline__ double stage_node(const StageParams& P, const double*
 }
 
 template <int D, int S, int KIND, int MODE>
-__global__ void __launch_bounds__(256, S == WENO5 ? 3 : 4) stage_kernel(const __grid_constant__ StageParams P) {
+__global__ void __launch_bounds__(256, 4) stage_kernel(const __grid_constant__ StageParams P) {
     const long long lidx = (long long)P.zlo * P.plane + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long idx = lidx >= (long long)P.zsplit * P.plane ? lidx + (long long)P.zskip * P.plane : lidx;
     unsigned long long kmin = ~0ull, kmax = 0ull, fz = ~0ull;
