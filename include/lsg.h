@@ -299,6 +299,14 @@ int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* op
 int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path);
 /* Raw CUDA stream (cudaStream_t) of the context, for external event timing. */
 int lsg_solver_stream(lsg_solver* s, void** stream);
+/* ---- diagnostics ------------------------------------------------------------
+ * Measured FP64 DADD/DMUL issue rate of the context's device (instructions/s):
+ * the second roofline of this FMA-free fp64 stencil, probed in the same run
+ * that reports against it (about 10 ms of device time). */
+int lsg_probe_fp64_rate(lsg_ctx* ctx, double* instr_per_s);
+/* Size of the context's NCCL communicator and this process's rank in it, read
+ * back from NCCL (ncclCommCount / ncclCommUserRank); 0 and -1 without one. */
+int lsg_ctx_comm_info(const lsg_ctx* ctx, int* nranks, int* rank);
 /* Kernels one lsg_solver_step launches. */
 int lsg_solver_launches_per_step(const lsg_solver* s, int* n);
 

@@ -36,6 +36,7 @@ EXPORTS = (
     "lsg_solver_step_host",
     "lsg_solver_step_timed",
     "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
+    "lsg_probe_fp64_rate", "lsg_ctx_comm_info",
 )
 
 _lib = None
@@ -131,6 +132,29 @@ class Context:
     def synchronize(self):
         call("lsg_ctx_synchronize", self.h)
 
+    def fp64_rate(self):
+        """Measured FP64 DADD/DMUL issue rate of this device (instructions/s)."""
+        r = C.c_double()
+        call("lsg_probe_fp64_rate", self.h, C.byref(r))
+        return r.value
+
+    def comm_info(self):
+        """(nranks, rank) as the NCCL communicator reports them; (0, -1) without one."""
+        n, r = C.c_int(), C.c_int()
+        call("lsg_ctx_comm_info", self.h, C.byref(n), C.byref(r))
+        return n.value, r.value
+
+    def local_nodes(self, g):
+        """Nodes this process holds of grid g: the whole grid, or on a
+        multi-rank context this rank's slab along the last axis (the size of
+        the fields the solver-backed calls take and return)."""
+        N = node_count(g)
+        if self.nranks > 1:
+            n = g.counts[g.dim - 1]
+            _, nz = slab_partition(n, self.nranks, self.rank)
+            N = N // n * nz
+        return N
+
     def launches(self):
         n = C.c_uint64()
         call("lsg_ctx_launch_count", self.h, C.byref(n))
@@ -161,7 +185,9 @@ class Context:
 
     def term_lf(self, g, p, t, v):
         v = np.ascontiguousarray(v, dtype=np.float64)
-        out = np.empty(node_count(g), dtype=np.float64)
+        out = np.empty(self.local_nodes(g), dtype=np.float64)
+        if v.size != out.size:
+            raise ValueError("term_lf: field size does not match the (local) node count")
         b = C.c_double()
         call("lsg_term_lf", self.h, C.byref(g), C.byref(p), C.c_double(t), abi.dptr(v), abi.dptr(out), C.byref(b))
         return out, b.value
@@ -212,7 +238,9 @@ class Context:
 
     def solve_brt(self, g, p, v0, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=4096):
         v0 = np.ascontiguousarray(v0, dtype=np.float64)
-        N = node_count(g)
+        N = self.local_nodes(g)
+        if v0.size != N:
+            raise ValueError("solve_brt: field size does not match the (local) node count")
         ck = np.empty(max(1, n_checkpoints) * N, dtype=np.float64)
         times = np.empty(max(1, n_checkpoints), dtype=np.float64)
         n_out = C.c_int()

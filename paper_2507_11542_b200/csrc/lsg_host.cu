@@ -1050,14 +1050,12 @@ void enqueue_step(lsg_solver* s, double dt, unsigned long long* range, cudaEvent
     if (s->method == LSG_CFL1) {
         const int b = 1 - a;
         run_stage(s, MODE_EULER, a, -1, b, dt, 0.0, range);
-        mark(1);
         s->cur = b;
     } else if (s->method == LSG_CFL2) {
         const int b = 1 - a;
         run_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
         mark(1);
         run_stage(s, MODE_COMBINE, b, a, a, dt, 0.5, range);
-        mark(2);
     } else {
         const int b = (a + 1) % 3, c = (a + 2) % 3;
         run_stage(s, MODE_EULER, a, -1, b, dt, 0.0, nullptr);
@@ -1065,8 +1063,12 @@ void enqueue_step(lsg_solver* s, double dt, unsigned long long* range, cudaEvent
         run_stage(s, MODE_COMBINE, b, a, c, dt, 0.25, nullptr);
         mark(2);
         run_stage(s, MODE_COMBINE, c, a, a, dt, 2.0 / 3.0, range);
-        mark(3);
     }
+    // the step ends when its last exchange (the next step's halo) has landed:
+    // the main stream joins the communication stream, so an event recorded
+    // after the step (bench timing, step_timed) covers the halo traffic too
+    join_comm(s);
+    mark(s->method + 1);
 }
 
 int stages_of(int method) { return method + 1; }
@@ -1092,6 +1094,25 @@ lsg_opts default_opts() {
 
 double smin(double a, double b) { return (b < a) ? b : a; }  // std::min
 
+// An invalid dissipation bound, reported as term_lax_friedrichs does: H is
+// evaluated on the current field first and a non-finite H wins
+// (hamiltonian.cpp:37-56).  One TERM stage into a scratch buffer.
+[[noreturn]] void fail_bound_invalid(lsg_solver* s) {
+    lsg_ctx* ctx = s->ctx;
+    const int nbuf = s->method == LSG_CFL3 ? 3 : 2;
+    CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
+    run_stage(s, MODE_TERM, s->cur, -1, (s->cur + 1) % nbuf, 0.0, 0.0, nullptr);
+    if (s->distributed) {
+        join_comm(s);
+        NCCL_CHECK(ncclAllReduce(s->dflags.p, s->dflags.p, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
+    }
+    unsigned flags = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof flags, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (flags & FLAG_HAM_NONFINITE) fail(LSG_ENUMERIC, "term_lax_friedrichs: hamiltonian produced a non-finite value");
+    fail(LSG_ENUMERIC, "term_lax_friedrichs: dissipation bound must be finite and non-negative");
+}
+
 // The dt schedule of one leg of run_cfl (integrator.cpp:22-97), host only:
 // alpha and the CFL bound are v-independent, so every step's (t, dt) follows
 // from (t0, tf, options) alone.  Validation errors are raised in the
@@ -1100,6 +1121,7 @@ struct LegPlan {
     std::vector<lsg_steplog> log;
     double t_final = 0.0;
     bool collapsed = false;
+    bool bound_invalid = false;  // raised by run_leg once H has been checked on the leg's field
 };
 
 LegPlan plan_leg(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in) {
@@ -1113,7 +1135,12 @@ LegPlan plan_leg(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in) {
     const double eps_stop = o.termination_epsilon * std::abs(tf);
     double t = t0;
     if (!(tf - t > 0.0 && tf - t >= eps_stop)) return plan;
-    check_alpha_valid(s);  // the first term evaluation validates the bounds
+    // the first term evaluation validates the bounds, after H (run_leg)
+    ensure_alpha(s);
+    if (s->alpha_flags & FLAG_BOUND_INVALID) {
+        plan.bound_invalid = true;
+        return plan;
+    }
     while (tf - t > 0.0 && tf - t >= eps_stop) {
         double target = tf;
         if (o.n_checkpoint_times) {
@@ -1141,6 +1168,7 @@ LegPlan plan_leg(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in) {
 // enqueued back to back, one synchronisation at the end for the per-step v
 // range and the error flags.
 void run_leg(lsg_solver* s, LegPlan& plan) {
+    if (plan.bound_invalid) fail_bound_invalid(s);
     std::vector<lsg_steplog>& log = plan.log;
     const bool collapsed = plan.collapsed;
     const long long nsteps = static_cast<long long>(log.size());
@@ -1729,6 +1757,10 @@ int lsg_term_lf(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, double t,
         ensure_alpha(s);
         CUDA_CHECK(cudaMemsetAsync(s->dflags.p, 0, sizeof(unsigned), ctx->stream));
         run_stage(s, MODE_TERM, 0, -1, 1, 0.0, 0.0, nullptr);  // halo exchange first on a multi-rank context
+        if (s->distributed) {  // every rank raises the same error
+            join_comm(s);
+            NCCL_CHECK(ncclAllReduce(s->dflags.p, s->dflags.p, 1, ncclUint32, ncclMax, ctx->comm, ctx->stream));
+        }
         unsigned flags = 0;
         CUDA_CHECK(cudaMemcpyAsync(&flags, s->dflags.p, sizeof flags, cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -1877,7 +1909,7 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
             plans.push_back(plan_leg(s, t, t_end, opts));
             t = plans.back().t_final;
             total += plans.back().log.size();
-            if (plans.back().collapsed) break;
+            if (plans.back().collapsed || plans.back().bound_invalid) break;
         }
         check_log_room(total, steps, log_cap, n_steps);
         upload(s, v0, 0);
@@ -2067,6 +2099,7 @@ int lsg_solver_step(lsg_solver* s, double t, double dt) {
     (void)t;
     return guarded([&] {
         if (!s) fail(LSG_EINVAL, "null solver");
+        activate(s->ctx);
         check_alpha_valid(s);
         if (s->ring_next >= s->range_cap) ensure_range(s, s->range_cap);
         enqueue_step(s, dt, s->drange.as<unsigned long long>() + kRangeWords * s->ring_next);
@@ -2163,6 +2196,49 @@ int lsg_solver_stream(lsg_solver* s, void** stream) {
     return guarded([&] {
         if (!s || !stream) fail(LSG_EINVAL, "stream: null argument");
         *stream = reinterpret_cast<void*>(s->ctx->stream);
+    });
+}
+
+int lsg_probe_fp64_rate(lsg_ctx* ctx, double* instr_per_s) {
+    return guarded([&] {
+        if (!instr_per_s) fail(LSG_EINVAL, "probe: null output");
+        activate(ctx);
+        int sms = 0;
+        CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        const int blocks = sms * 8, iters = 4000;
+        DevBuf out;
+        out.alloc(sizeof(double) * static_cast<size_t>(blocks) * 256, ctx->stream);
+        cudaEvent_t e0, e1;
+        CUDA_CHECK(cudaEventCreate(&e0));
+        CUDA_CHECK(cudaEventCreate(&e1));
+        double best = 0.0;
+        for (int rep = 0; rep < 3; ++rep) {  // the first run warms clocks and caches
+            CUDA_CHECK(cudaEventRecord(e0, ctx->stream));
+            launch_fp64_rate(out.as<double>(), blocks, iters, ctx->stream);
+            ctx->note_launch();
+            CUDA_CHECK(cudaEventRecord(e1, ctx->stream));
+            CUDA_CHECK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+            const double ops = static_cast<double>(blocks) * 256.0 * iters * 8.0;
+            if (rep > 0) best = std::max(best, ops / (ms * 1e-3));
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        out.release();
+        *instr_per_s = best;
+    });
+}
+
+int lsg_ctx_comm_info(const lsg_ctx* ctx, int* nranks, int* rank) {
+    return guarded([&] {
+        if (!ctx || !nranks || !rank) fail(LSG_EINVAL, "comm_info: null argument");
+        *nranks = 0;
+        *rank = -1;
+        if (ctx->comm) {
+            NCCL_CHECK(ncclCommCount(ctx->comm, nranks));
+            NCCL_CHECK(ncclCommUserRank(ctx->comm, rank));
+        }
     });
 }
 

@@ -189,3 +189,27 @@ __global__ void stamp_kernel(unsigned long long* out) {
 }
 void launch_stamp(unsigned long long* out, cudaStream_t st) { stamp_kernel<<<1, 1, 0, st>>>(out); }
 }  // namespace lsg
+
+namespace lsg {
+// FP64 issue-rate probe (the second roofline of the stencil, measured in the
+// run that reports against it): 8 independent DADD/DMUL chains per thread,
+// 8 blocks of 256 threads per SM; one op per chain and iteration (iters even).
+__global__ void __launch_bounds__(256) fp64_rate_kernel(double* out, int iters, double a, double b) {
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < iters; i += 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = __dmul_rn(r[k], b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += r[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+void launch_fp64_rate(double* out, int blocks, int iters, cudaStream_t st) {
+    fp64_rate_kernel<<<blocks, 256, 0, st>>>(out, iters, 1e-9, 1.0000001);
+}
+}  // namespace lsg

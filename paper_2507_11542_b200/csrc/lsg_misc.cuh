@@ -66,6 +66,8 @@ void launch_shape(const ShapeParams& S, cudaStream_t st);
 // elementwise set operations (implicit_surfaces.cpp:128-151): op 1 min, 2 max, 3 negate a
 void launch_set_op(int op, long long n, const double* a, const double* b, double* out, cudaStream_t st);
 void launch_stamp(unsigned long long* out, cudaStream_t st);  // %globaltimer into *out (tracing)
+// blocks x 256 threads x 8 chains x iters FP64 DADD/DMUL (lsg_probe_fp64_rate)
+void launch_fp64_rate(double* out, int blocks, int iters, cudaStream_t st);
 void launch_range_init(unsigned long long* r, long long nslots, cudaStream_t st);
 long long zero_set_2d(const double* f, int nx, int ny, const double* ax, const double* ay, double dx, double dy,
                       double* seg_dev, long long cap, int* scratch_counts, int* scratch_offsets, void* temp,

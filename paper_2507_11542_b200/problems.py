@@ -72,10 +72,14 @@ def cfg4_dubins6(n=41, scheme=abi.SCHEME_WENO5):
     return Setup("cfg4_dubins6", g, p, abi.CFL3, (0.0, 0.5), (PAIR_DISTANCE, [0.0] * 6, 0.25, ()))
 
 
-def cfg5_normal(n=512, scheme=abi.SCHEME_WENO5, z_scale=1):
+def cfg5_normal(n=512, scheme=abi.SCHEME_WENO5, z_scale=1, nz=None):
     """3-D motion in the normal direction on a periodic box (configs[4]; the
-    reference has no curvature operator, so only the |grad v| term)."""
-    nz = n * z_scale
+    reference has no curvature operator, so only the |grad v| term).
+
+    z_scale > 1 stacks z_scale boxes along z (weak scaling: 512 x 512 x 512*N);
+    nz overrides the plane count at the same spacing (a thin periodic slab of
+    the same lines and strides, the CPU baseline's bounded sample)."""
+    nz = n * z_scale if nz is None else nz
     h = 2.0 / n
     g = _grid([-1.0, -1.0, -1.0], [1.0 - h, 1.0 - h, -1.0 + h * (nz - 1)], [n, n, nz], periodic=(0, 1, 2))
     p = abi.make_problem(abi.HAM_NORMAL, scheme, [1.0])
