@@ -321,12 +321,12 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2) march3_kernel(const __
                     wx[j] = v.x;
                     wx[j + 1] = v.y;
                 }
-                line_lr<S>(wx + SH, P.lc[0], L, R);
+                double L2, R2;
+                line_lr2<S>(wx + SH, P.lc[0], L, R, L2, R2);
                 pa[0] = 0.5 * (L + R);
                 da += P.alpha[0] * (R - L);
-                line_lr<S>(wx + SH + 1, P.lc[0], L, R);
-                pb[0] = 0.5 * (L + R);
-                db += P.alpha[0] * (R - L);
+                pb[0] = 0.5 * (L2 + R2);
+                db += P.alpha[0] * (R2 - L2);
             }
             double ca, cb;  // centre values
             {   // y: one 128-bit load per row gives both nodes' windows

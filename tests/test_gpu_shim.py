@@ -47,3 +47,18 @@ def test_divmod_index_exact():
     out = subprocess.run([binary], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "divmod ok" in out.stdout
+
+
+@pytest.mark.gpu
+def test_weno5_exact_blocks_bitwise():
+    """The exact WENO5's select-free constant divisions and the shared-quotient
+    two-node form (line_lr2<WENO5>) equal the reference's IEEE arithmetic bit
+    for bit on ~1e9 random operands and ~2e8 random windows, including zeros,
+    flat runs, subnormal-adjacent and overflowing differences
+    (tests/cpp/weno5_check.cu; spatial_derivatives.cpp:78-97)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    binary = os.path.join(root, "tests", "cpp", "weno5_check")
+    assert os.path.exists(binary), "tests/cpp/weno5_check not built: run __graft_entry__.build()"
+    out = subprocess.run([binary], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "weno5 ok" in out.stdout
