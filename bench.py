@@ -692,7 +692,15 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=90.0)
     ap.add_argument("--dist-selftest", action="store_true",
                     help="under torchrun with one rank: run the multi-rank (NCCL) branch on a one-rank communicator")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="each rank prints its rank / world size and exits (tests the --gpus N launcher on CPU)")
     args = ap.parse_args()
+    if args.launch_check and "WORLD_SIZE" in os.environ:
+        ws, rank, local = dist_env()
+        print(json.dumps({"launch_check": True, "rank": rank, "world_size": ws, "local_rank": local,
+                          "master_addr": os.environ.get("MASTER_ADDR"), "nccl_debug": os.environ.get("NCCL_DEBUG")}),
+              flush=True)
+        return 0
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
     if args.impl == "b200" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -294,9 +294,17 @@ int lsg_solver_step_timed(lsg_solver* s, double t, double dt, double* stage_ms, 
 /* run_cfl over [t0, tf] with the reference's step control (integrator.cpp:22-97). */
 int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* opts,
                          lsg_steplog* steps, size_t log_cap, size_t* n_steps, double* t_final);
-/* Snapshot of the resident value function (this rank's slab in a distributed
- * context, written with the slab's own sub-grid header). */
+/* Snapshot of the resident value function in the reference's format
+ * (snapshot.cpp:68-93).  In a distributed context the call is collective: the
+ * slabs are gathered on rank 0 (NCCL point-to-point, 1 GiB chunks), which
+ * writes the whole grid to `path`; the other ranks write nothing (their path
+ * may be NULL). */
 int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path);
+/* Gather a distributed field held as host slabs (e.g. solve_brt's per-rank
+ * checkpoints) into global_out on rank 0 (node_count(g) doubles; unused and
+ * may be NULL elsewhere).  Collective on a multi-rank context; a plain copy
+ * otherwise. */
+int lsg_gather_field(lsg_ctx* ctx, const lsg_grid* g, const double* local, double* global_out);
 /* Raw CUDA stream (cudaStream_t) of the context, for external event timing. */
 int lsg_solver_stream(lsg_solver* s, void** stream);
 /* ---- diagnostics ------------------------------------------------------------

@@ -36,7 +36,7 @@ EXPORTS = (
     "lsg_solver_step_host",
     "lsg_solver_step_timed",
     "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
-    "lsg_probe_fp64_rate", "lsg_ctx_comm_info",
+    "lsg_probe_fp64_rate", "lsg_ctx_comm_info", "lsg_gather_field",
 )
 
 _lib = None
@@ -236,7 +236,19 @@ class Context:
             raise_for(rc)
             return v, _steps(log, n.value, log_cap), tfin.value
 
-    def solve_brt(self, g, p, v0, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=4096):
+    def gather_field(self, g, local):
+        """Global field on rank 0 from this rank's slab (lsg_gather_field;
+        collective on a multi-rank context, None on the other ranks)."""
+        local = np.ascontiguousarray(local, dtype=np.float64)
+        root = self.nranks <= 1 or self.rank == 0
+        out = np.empty(node_count(g), dtype=np.float64) if root else None
+        call("lsg_gather_field", self.h, C.byref(g), abi.dptr(local), abi.dptr(out) if root else None)
+        return out
+
+    def solve_brt(self, g, p, v0, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=4096, gather=False):
+        """solve_brt (reachability.cpp:135-174).  On a multi-rank context v0 and
+        the checkpoints are this rank's slab; gather=True returns whole-grid
+        checkpoints on rank 0 instead (None on the other ranks)."""
         v0 = np.ascontiguousarray(v0, dtype=np.float64)
         N = self.local_nodes(g)
         if v0.size != N:
@@ -258,7 +270,11 @@ class Context:
             raise_for(rc)
             break
         k = n_out.value
-        return ck[: k * N].reshape(k, N), times[:k].copy(), _steps(log, n.value, log_cap), secs.value
+        ck = ck[: k * N].reshape(k, N)
+        if gather and self.nranks > 1:
+            full = [self.gather_field(g, ck[j]) for j in range(k)]
+            ck = np.stack(full) if self.rank == 0 else None
+        return ck, times[:k].copy(), _steps(log, n.value, log_cap), secs.value
 
 
     def extract_zero_set_2d(self, g, field):
@@ -407,7 +423,9 @@ class Solver:
             return _steps(log, n.value, log_cap), tfin.value
 
     def write_snapshot(self, time, path):
-        call("lsg_solver_write_snapshot", self.h, C.c_double(time), str(path).encode())
+        """Reference-format snapshot of the resident field; collective on a
+        multi-rank context (rank 0 writes the whole grid)."""
+        call("lsg_solver_write_snapshot", self.h, C.c_double(time), str(path).encode() if path is not None else None)
 
     def stream(self):
         p = C.c_void_p()

@@ -1256,6 +1256,63 @@ void download(lsg_solver* s, double* host, int b) {
     CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
 }
 
+// Gather the slabs of a distributed field into global_host on rank 0 (the
+// slab axis is the slowest, so the global column-major array is the slabs
+// concatenated in rank order; reachability.cpp:160-170, snapshot.cpp:68-93).
+// Each rank passes its slab as a device pointer (dev_local) or a host
+// pointer (host_local).  Point-to-point NCCL in 1 GiB chunks through one
+// device staging buffer; ranks other than 0 only send.  Collective.
+void gather_to_root(lsg_ctx* ctx, const lsg_grid* g, const double* dev_local, const double* host_local,
+                    double* global_host) {
+    const int D = g->dim, P = ctx->nranks, me = ctx->rank;
+    long long plane = 1;
+    for (int d = 0; d + 1 < D; ++d) plane *= g->counts[d];
+    const long long chunk = 1LL << 27;  // doubles (1 GiB)
+    DevBuf stage;
+    auto slab_of = [&](int r, long long* off, long long* n) {
+        int z0 = 0, nz = 0;
+        partition(g->counts[D - 1], P, r, &z0, &nz);
+        *off = static_cast<long long>(z0) * plane;
+        *n = static_cast<long long>(nz) * plane;
+    };
+    long long off = 0, n = 0;
+    slab_of(me, &off, &n);
+    if (me == 0) {
+        if (dev_local)
+            CUDA_CHECK(cudaMemcpyAsync(global_host + off, dev_local, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                       ctx->stream));
+        else
+            std::memcpy(global_host + off, host_local, sizeof(double) * n);
+        for (int r = 1; r < P; ++r) {
+            long long ro = 0, rn = 0;
+            slab_of(r, &ro, &rn);
+            for (long long k = 0; k < rn; k += chunk) {
+                const long long c = std::min(chunk, rn - k);
+                if (stage.bytes < sizeof(double) * static_cast<size_t>(c)) stage.alloc(sizeof(double) * c, ctx->stream);
+                NCCL_CHECK(ncclRecv(stage.p, static_cast<size_t>(c), ncclFloat64, r, ctx->comm, ctx->stream));
+                CUDA_CHECK(cudaMemcpyAsync(global_host + ro + k, stage.p, sizeof(double) * c, cudaMemcpyDeviceToHost,
+                                           ctx->stream));
+                CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            }
+        }
+    } else {
+        for (long long k = 0; k < n; k += chunk) {
+            const long long c = std::min(chunk, n - k);
+            const double* src = dev_local ? dev_local + k : nullptr;
+            if (!dev_local) {
+                if (stage.bytes < sizeof(double) * static_cast<size_t>(c)) stage.alloc(sizeof(double) * c, ctx->stream);
+                CUDA_CHECK(cudaMemcpyAsync(stage.p, host_local + k, sizeof(double) * c, cudaMemcpyHostToDevice,
+                                           ctx->stream));
+                src = stage.as<double>();
+            }
+            NCCL_CHECK(ncclSend(src, static_cast<size_t>(c), ncclFloat64, 0, ctx->comm, ctx->stream));
+            CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        }
+    }
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    stage.release();
+}
+
 // One step with the field coming from and going back to host memory, the
 // copies overlapped with the stage kernels (lsg_solver_step_host).  The input
 // is uploaded in K chunks of planes along the last axis on a copy-in stream.
@@ -2172,23 +2229,39 @@ int lsg_solver_integrate(lsg_solver* s, double t0, double tf, const lsg_opts* op
 int lsg_solver_write_snapshot(lsg_solver* s, double time, const char* path) {
     return guarded([&] {
         if (!s) fail(LSG_EINVAL, "null solver");
-        if (!path) fail(LSG_EINVAL, "write_snapshot: null path");
         activate(s->ctx);
-        lsg_grid g = s->g;
-        size_t n = static_cast<size_t>(s->total);
-        if (s->distributed) {  // this rank's slab as its own sub-grid
-            const Slab& sl = s->slabs[0];
-            const int D = s->D;
-            const double dz = spacing(&s->g, D - 1);
-            g.counts[D - 1] = sl.nz;
-            g.mins[D - 1] = s->g.mins[D - 1] + static_cast<double>(sl.z0) * dz;
-            g.maxs[D - 1] = s->g.mins[D - 1] + static_cast<double>(sl.z0 + sl.nz - 1) * dz;
-            n = static_cast<size_t>(sl.nodes);
+        const size_t n = static_cast<size_t>(s->total);
+        if (s->distributed) {  // collective: the slabs gathered on rank 0, which writes the whole grid
+            if (s->ctx->rank == 0 && !path) fail(LSG_EINVAL, "write_snapshot: null path");
+            join_comm(s);
+            std::vector<double> host(s->ctx->rank == 0 ? n : 0);
+            gather_to_root(s->ctx, &s->g, s->slabs[0].f[s->cur], nullptr, host.data());
+            if (s->ctx->rank == 0) {
+                const int rc = lsg_write_snapshot(&s->g, host.data(), time, path);
+                if (rc) fail(rc, g_err);
+            }
+            return;
         }
+        if (!path) fail(LSG_EINVAL, "write_snapshot: null path");
         std::vector<double> host(n);
         download(s, host.data(), s->cur);
-        const int rc = lsg_write_snapshot(&g, host.data(), time, path);
+        const int rc = lsg_write_snapshot(&s->g, host.data(), time, path);
         if (rc) fail(rc, g_err);
+    });
+}
+
+int lsg_gather_field(lsg_ctx* ctx, const lsg_grid* g, const double* local, double* global_out) {
+    return guarded([&] {
+        activate(ctx);
+        check_grid(g);
+        if (!local) fail(LSG_EINVAL, "gather_field: null local slab");
+        if (ctx->nranks <= 1 || !ctx->comm) {  // one rank: the slab is the field
+            if (!global_out) fail(LSG_EINVAL, "gather_field: null output");
+            if (global_out != local) std::memcpy(global_out, local, sizeof(double) * static_cast<size_t>(node_count(g)));
+            return;
+        }
+        if (ctx->rank == 0 && !global_out) fail(LSG_EINVAL, "gather_field: null output on rank 0");
+        gather_to_root(ctx, g, nullptr, local, global_out);
     });
 }
 
