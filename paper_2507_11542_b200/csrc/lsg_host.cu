@@ -278,6 +278,50 @@ March3Fn lookup_march3(int kind, int scheme, int mode, bool range) {
     return nullptr;
 }
 
+March3TmaFn lookup_march3_tma(int kind, int scheme, int mode, bool range) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return march3_tma_lookup_linear(scheme, mode, range);
+        case LSG_HAM_NORMAL: return march3_tma_lookup_normal(scheme, mode, range);
+        case LSG_HAM_ROCKETS: return march3_tma_lookup_rockets(scheme, mode, range);
+        case LSG_HAM_AIR3D: return march3_tma_lookup_air3d(scheme, mode, range);
+    }
+    return nullptr;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return static_cast<EncodeTiledFn>(nullptr);
+        }
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// 3-D fp64 tensor map over a slab buffer of n0 x n1 x nz doubles (plane -halo
+// first), box bx x by x 1, zero fill outside.
+CUtensorMap tensor_map_3d(const double* base, int n0, int n1, int nz, int bx, int by) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(n0), static_cast<cuuint64_t>(n1), static_cast<cuuint64_t>(nz)};
+    const cuuint64_t strides[2] = {sizeof(double) * static_cast<cuuint64_t>(n0),
+                                   sizeof(double) * static_cast<cuuint64_t>(n0) * static_cast<cuuint64_t>(n1)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(bx), static_cast<cuuint32_t>(by), 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(LSG_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
+}
+
 Box3Fn lookup_box3(int kind, int scheme, int mode, bool range) {
     switch (kind) {
         case LSG_HAM_LINEAR: return box3_lookup_linear(scheme, mode, range);
@@ -360,6 +404,7 @@ struct Slab {
     long long nodes = 0;
     March3 m3{};       // 2.5-D tiling of this slab (3-D grids)
     dim3 m3_grid;
+    CUtensorMap tmu[3], tmv[3];  // march3_tma_kernel: tile box / v0 box over each buffer
     DevBuf buf[3];
     double* f[3] = {nullptr, nullptr, nullptr};  // plane 0 of each buffer
 };
@@ -392,9 +437,11 @@ struct lsg_solver {
     double bound = 0.0;
     StageFn fn[3] = {nullptr, nullptr, nullptr};
     March3Fn m3fn[3][2] = {};  // [mode][with v-range reduction]
+    March3TmaFn m3tfn[3][2] = {};  // TMA-fed variant (even rows; LSG_TMA=0 disables)
     Box3Fn b3fn[3][2] = {};
     int m3_threads = 0;
     int m3_pitch = 0;
+    int m3_slot = 0, m3_vslot = 0, m3_hmax = 0;  // march3_tma_kernel ring geometry
     int m3_per_sm = 1;
     int div31_mask = 3;  // LSG_DIV31: which divmod31 paths slab_params may enable (tests)
     size_t m3_smem = 0;
@@ -590,9 +637,39 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                             CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->m3fn[m][r]),
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                             static_cast<int>(s->m3_smem)));
+                // TMA-fed tiles where rows are 16-byte multiples and the boxes fit
+                const char* te = std::getenv("LSG_TMA");
+                const int rows_box = R + 2 * Wr;
+                if (!(te && std::string(te) == "0") && n0 % 2 == 0 && s->m3_pitch <= 256 && rows_box <= 256 &&
+                    TX <= 256 && R <= 256 && encode_tiled()) {
+                    bool allt = true;
+                    for (int m = 0; m < 3; ++m)
+                        for (int r = 0; r < 2; ++r) {
+                            s->m3tfn[m][r] = lookup_march3_tma(p->kind, kscheme, m, r == 1);
+                            allt = allt && s->m3tfn[m][r];
+                        }
+                    if (allt) {
+                        s->m3_slot = ((s->m3_pitch * rows_box + 15) / 16) * 16;
+                        s->m3_vslot = ((TX * R + 15) / 16) * 16;
+                        s->m3_hmax = 2 * Wr * (TX + R);
+                        s->m3_smem = sizeof(double) * static_cast<size_t>(NB * s->m3_slot + NV * s->m3_vslot +
+                                                                          (2 + 1) * s->m3_hmax) +
+                                     sizeof(unsigned long long) * NB + 128;  // + alignment slack
+                        for (int m = 0; m < 3; ++m)
+                            for (int r = 0; r < 2; ++r)
+                                CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->m3tfn[m][r]),
+                                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                static_cast<int>(s->m3_smem)));
+                    } else {
+                        for (auto& fm : s->m3tfn) fm[0] = fm[1] = nullptr;
+                    }
+                }
                 int per_sm = 0;
                 CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                    &per_sm, reinterpret_cast<const void*>(s->m3fn[2][1]), threads, s->m3_smem));
+                    &per_sm,
+                    s->m3tfn[2][1] ? reinterpret_cast<const void*>(s->m3tfn[2][1])
+                                   : reinterpret_cast<const void*>(s->m3fn[2][1]),
+                    threads, s->m3_smem));
                 s->m3_per_sm = std::max(1, per_sm);
             } else {
                 for (auto& fm : s->m3fn) fm[0] = fm[1] = nullptr;
@@ -631,15 +708,21 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                 nzc = (sl.nz + chunk - 1) / chunk;
             }
             if (std::getenv("LSG_M3_VERBOSE"))
-                std::fprintf(stderr, "march3: TX=%d R=%d tiles=%d chunks=%d blocks/SM=%d smem=%zu threads=%d\n", TX, R,
-                             nt, nzc, s->m3_per_sm, s->m3_smem, s->m3_threads);
-            sl.m3 = March3{TX, R, ntx, nzc, s->m3_pitch};
+                std::fprintf(stderr, "march3%s: TX=%d R=%d tiles=%d chunks=%d blocks/SM=%d smem=%zu threads=%d\n",
+                             s->m3tfn[0][0] ? " (TMA)" : "", TX, R, nt, nzc, s->m3_per_sm, s->m3_smem, s->m3_threads);
+            sl.m3 = March3{TX, R, ntx, nzc, s->m3_pitch, s->m3_slot, s->m3_vslot, s->m3_hmax};
             sl.m3_grid = dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nzc));
         }
         const long long padded = static_cast<long long>(sl.nz + 2 * s->halo_w) * s->plane;
         for (int b = 0; b < nbuf; ++b) {
             sl.buf[b].alloc(sizeof(double) * static_cast<size_t>(padded), ctx->stream);
             sl.f[b] = sl.buf[b].as<double>() + static_cast<long long>(s->halo_w) * s->plane;
+            if (s->m3tfn[0][0]) {
+                const int nzp = sl.nz + 2 * s->halo_w;
+                sl.tmu[b] = tensor_map_3d(sl.buf[b].as<double>(), g->counts[0], g->counts[1], nzp, s->m3_pitch,
+                                          sl.m3.R + 2 * s->W);
+                sl.tmv[b] = tensor_map_3d(sl.buf[b].as<double>(), g->counts[0], g->counts[1], nzp, sl.m3.TX, sl.m3.R);
+            }
         }
         s->slabs.push_back(std::move(sl));
     }
@@ -947,7 +1030,7 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         }
         if (zskip) M.nzc = 2;  // one chunk per band: none straddles the gap
         const dim3 grid(sl.m3_grid.x, static_cast<unsigned>(M.nzc));
-        void* args[] = {&P, &M};
+        void* args[] = {&P, &M, &sl.tmu[ui], &sl.tmv[vi >= 0 ? vi : ui]};
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(static_cast<unsigned>(s->m3_threads));
@@ -958,7 +1041,9 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         attr[0].val.programmaticStreamSerializationAllowed = s->pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]), args));
+        const void* fn = s->m3tfn[mode][0] ? reinterpret_cast<const void*>(s->m3tfn[mode][range ? 1 : 0])
+                                           : reinterpret_cast<const void*>(s->m3fn[mode][range ? 1 : 0]);
+        CUDA_CHECK(cudaLaunchKernelExC(&cfg, fn, args));
     } else {
         void* args[] = {&P};
         const long long n = static_cast<long long>(zhi - zlo) * s->plane;

@@ -33,6 +33,10 @@ March3Fn march3_lookup_linear(int s, int m, bool range);
 March3Fn march3_lookup_normal(int s, int m, bool range);
 March3Fn march3_lookup_rockets(int s, int m, bool range);
 March3Fn march3_lookup_air3d(int s, int m, bool range);
+March3TmaFn march3_tma_lookup_linear(int s, int m, bool range);
+March3TmaFn march3_tma_lookup_normal(int s, int m, bool range);
+March3TmaFn march3_tma_lookup_rockets(int s, int m, bool range);
+March3TmaFn march3_tma_lookup_air3d(int s, int m, bool range);
 
 StageFn stage_lookup_linear(int D, int s, int m);
 StageFn stage_lookup_normal(int D, int s, int m);
