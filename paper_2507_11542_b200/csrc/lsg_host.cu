@@ -22,6 +22,7 @@
 // and overlapped with the stage kernels).
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges cost nothing unless a tool is attached
 
 #include <algorithm>
 #include <chrono>
@@ -250,6 +251,19 @@ struct lsg_ctx {
 
 namespace {
 
+// NVTX range around host-side enqueue work (tracing): the names
+// tie a profiler timeline's launches to the reference's loop structure
+// (integrator.cpp:58-85 stages, reachability.cpp:160-170 legs).
+struct NvtxRange {
+    bool on;
+    NvtxRange(bool enabled, const char* name) : on(enabled) {
+        if (on) nvtxRangePushA(name);
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+};
+
 void activate(lsg_ctx* ctx) {
     if (!ctx) fail(LSG_EINVAL, "null context");
     CUDA_CHECK(cudaSetDevice(ctx->device));
@@ -386,6 +400,25 @@ int kind_dim(int kind) {
     return 0;
 }
 
+// Whether a kind's Hamiltonian and dissipation bound are independent of t.
+// The reference evaluates alpha at every stage time (hamiltonian.cpp:44-56);
+// the device computes it once per solver and plans a leg's dt schedule up
+// front, which is exact only for time-invariant kinds.  Every device kind is;
+// a time-dependent kind must recompute alpha per stage time instead, and
+// ensure_alpha refuses it until it does.
+bool kind_time_invariant(int kind) {
+    switch (kind) {
+        case LSG_HAM_LINEAR:
+        case LSG_HAM_ROTATION:
+        case LSG_HAM_ROCKETS:
+        case LSG_HAM_AIR3D:
+        case LSG_HAM_DBLINT4:
+        case LSG_HAM_DUBINS6:
+        case LSG_HAM_NORMAL: return true;
+    }
+    return false;
+}
+
 unsigned trig_dims(int kind) {
     switch (kind) {
         case LSG_HAM_ROCKETS: return 1u << 2;
@@ -452,6 +485,7 @@ struct lsg_solver {
     // whenever the field is written from outside a stage)
     bool halo_ok[3] = {false, false, false};
     bool pdl = true;  // programmatic dependent launch between stages (LSG_PDL=0 disables; read at creation)
+    bool nvtx = false;  // NVTX range per stage / exchange / leg (LSG_NVTX=1; read at creation)
     cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
     cudaStream_t side = nullptr;  // boundary bands, concurrent with the interior (slabs only)
     cudaStream_t cin = nullptr, cout = nullptr;  // lsg_solver_step_host copy streams (created on first use)
@@ -499,6 +533,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->W = ghost_width(p->scheme);
     s->distributed = ctx->nranks > 1 || ctx->dist_selftest;
     s->pdl = pdl_enabled();
+    if (const char* e = std::getenv("LSG_NVTX")) s->nvtx = std::string(e) == "1";
     if (const char* e = std::getenv("LSG_DIV31")) s->div31_mask = std::atoi(e) & 3;
     s->P = s->distributed ? ctx->nranks : nslabs;
     s->total = node_count(g);
@@ -869,6 +904,8 @@ void ensure_range(lsg_solver* s, long long nslots) {
 void ensure_alpha(lsg_solver* s) {
     if (s->alpha_done) return;
     if (!s->invalid.empty()) fail(LSG_EINVAL, s->invalid);
+    if (!kind_time_invariant(s->p.kind))
+        fail(LSG_EINVAL, "hamiltonian: time-dependent kinds need per-stage alpha (not implemented)");
     lsg_ctx* ctx = s->ctx;
     CUDA_CHECK(cudaMemsetAsync(s->dalpha.p, 0, s->dalpha.bytes, ctx->stream));
     AlphaFn fn = lookup_alpha(s->p.kind);
@@ -917,6 +954,7 @@ void check_alpha_valid(lsg_solver* s) {
 // in-process, NCCL send/recv across ranks); ring for a periodic last axis.
 void exchange(lsg_solver* s, int b, cudaStream_t st) {
     if (s->halo_w == 0) return;
+    NvtxRange nv(s->nvtx, "lsg halo exchange");
     lsg_ctx* ctx = s->ctx;
     const bool periodic = bc_of(&s->g, s->D - 1) == LSG_BC_PERIODIC;
     const long long w = s->halo_w;
@@ -1094,6 +1132,8 @@ void launch_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, do
 // has no valid halo and is exchanged before its first stage.
 void run_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, double c, unsigned long long* range) {
     lsg_ctx* ctx = s->ctx;
+    static const char* const names[3] = {"lsg term (TERM)", "lsg RK stage (EULER)", "lsg RK stage (COMBINE)"};
+    NvtxRange nv(s->nvtx, names[mode]);
     if (s->halo_w == 0) {
         launch_stage(s, mode, ui, vi, oi, dt, c, range, 0, ctx->stream);
         return;
@@ -1253,6 +1293,7 @@ LegPlan plan_leg(lsg_solver* s, double t0, double tf, const lsg_opts* opts_in) {
 // enqueued back to back, one synchronisation at the end for the per-step v
 // range and the error flags.
 void run_leg(lsg_solver* s, LegPlan& plan) {
+    NvtxRange nv(s->nvtx, "lsg leg (run_cfl)");
     if (plan.bound_invalid) fail_bound_invalid(s);
     std::vector<lsg_steplog>& log = plan.log;
     const bool collapsed = plan.collapsed;

@@ -1,0 +1,8 @@
+# full device evidence for the current build: GPU suite, smoke, bench (both arms), ncu captures
+set -x
+TAG=${1:-r2}
+python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/${TAG}_gputest.log; cat gpurun_out/${TAG}_gputest.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
+python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
+python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref rc=$?"
+bash tools/ncu_bench.sh ${TAG}

@@ -16,7 +16,8 @@ from collections import Counter
 FP64_OPS = {"DADD", "DMUL", "DFMA", "DSETP", "DMNMX"}
 
 
-SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+         "ns": 1e-3, "us": 1.0, "ms": 1e3}
 
 
 def raw(rep):

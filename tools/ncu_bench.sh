@@ -7,7 +7,7 @@
 TAG=${1:-r2}
 for sk in "weno5 3" "eno3 2" "weno5-fast 4"; do set -- $sk
   ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-      -k "regex:march3_kernelILi$2ELi7ELi2ELb0E" --launch-skip 1 -c 1 -o gpurun_out/${TAG}_cfg5_$1 -f \
+      -k "regex:march3_tma_kernelILi$2ELi7ELi2ELb0E" --launch-skip 1 -c 1 -o gpurun_out/${TAG}_cfg5_$1 -f \
       python bench.py --scheme $1 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-extras \
       > gpurun_out/${TAG}_ncu_$1.log 2>&1
   echo "ncu $1 rc=$?"
