@@ -35,6 +35,14 @@ for counts, per in [((21, 13, 11), (2,)), ((300, 9, 8), (0, 1)), ((7, 9, 12), ()
         run(g, p)
         run(g, p, nslabs=2)
         ctx.term_lf(g, p, 0.0, rng.uniform(-1, 1, _lib.node_count(g)))
+# TMA-fed tiles (even x extents): interior and border tiles, periodic and
+# extrapolated x/y/z (extrapolated ghost planes at a non-periodic z edge), slabs
+for counts, per in [((32, 20, 9), ()), ((64, 18, 10), (0, 1, 2)), ((40, 33, 8), (2,)), ((300, 9, 8), (1,))]:
+    g = abi.make_grid([-1, -1, -1], [1, 1, 1], list(counts), per)
+    for sch in range(4):
+        p = abi.make_problem(abi.HAM_LINEAR, sch, lin3, abi.GROW, True)
+        run(g, p)
+        run(g, p, nslabs=2)
 os.environ["LSG_KERNEL"] = "box3"
 g = abi.make_grid([-1, -1, -1], [1, 1, 1], [19, 11, 9], (2,))
 run(g, abi.make_problem(abi.HAM_LINEAR, abi.SCHEME_ENO3, lin3, abi.GROW, True))
