@@ -486,6 +486,11 @@ struct lsg_solver {
     bool halo_ok[3] = {false, false, false};
     bool pdl = true;  // programmatic dependent launch between stages (LSG_PDL=0 disables; read at creation)
     bool nvtx = false;  // NVTX range per stage / exchange / leg (LSG_NVTX=1; read at creation)
+    // halos: overlap the exchange with the interior (bands first on a side
+    // stream) for small slabs, or exchange before each stage's single launch
+    // for large ones, where the exchange is a small fraction of the stage and
+    // the extra band launch costs more than it hides (LSG_HALO_OVERLAP=0/1 forces)
+    bool overlap_halo = true;
     cudaStream_t comm = nullptr;  // halo-exchange stream (slabs only)
     cudaStream_t side = nullptr;  // boundary bands, concurrent with the interior (slabs only)
     cudaStream_t cin = nullptr, cout = nullptr;  // lsg_solver_step_host copy streams (created on first use)
@@ -539,6 +544,11 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->total = node_count(g);
     for (int d = 0; d + 1 < s->D; ++d) s->plane *= g->counts[d];
     s->halo_w = (s->P > 1 || s->distributed) ? s->W : 0;
+    {
+        const long long slab_nodes = s->total / std::max(1, s->P);
+        s->overlap_halo = slab_nodes < (32LL << 20);  // 32 Mi nodes: ~0.4-4 ms stages vs ~20-40 us exchanges
+        if (const char* e = std::getenv("LSG_HALO_OVERLAP")) s->overlap_halo = std::string(e) != "0";
+    }
     if (s->halo_w) {
         // halo traffic and boundary bands sit on the critical path of the next
         // stage: their blocks go ahead of the interior's when SMs free up
@@ -1062,7 +1072,10 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         March3 M = sl.m3;
         if (zhi - zlo < sl.nz)  // a partial range: chunks of >= 3 planes
             M.nzc = std::max(1, std::min(M.nzc, (zhi - zlo) / 3));
-        if (reserve_blocks > 0) {  // share one wave with a concurrent launch (the boundary bands)
+        if (reserve_blocks > 0 && 2 * reserve_blocks <= 148 * s->m3_per_sm) {
+            // share one wave with a concurrent launch (the boundary bands) when
+            // the bands are a small part of a wave; with many tiles they are not,
+            // and the interior keeps its balanced chunks
             const int slots = 148 * s->m3_per_sm - reserve_blocks;
             M.nzc = std::max(1, std::min(M.nzc, slots / std::max(1, static_cast<int>(sl.m3_grid.x))));
         }
@@ -1144,6 +1157,16 @@ void run_stage(lsg_solver* s, int mode, int ui, int vi, int oi, double dt, doubl
         exchange(s, b, s->comm);
         CUDA_CHECK(cudaEventRecord(s->ev_halo, s->comm));
     };
+    if (!s->overlap_halo) {  // large slabs: exchange u's halo, then one launch over all planes
+        if (!s->halo_ok[ui]) {
+            join_comm(s);
+            exchange(s, ui, ctx->stream);
+            s->halo_ok[ui] = true;
+        }
+        launch_stage(s, mode, ui, vi, oi, dt, c, range, 0, ctx->stream);
+        s->halo_ok[oi] = false;
+        return;
+    }
     if (!s->halo_ok[ui]) {
         exchange_after(s->ev_ready, ctx->stream, ui);
         s->halo_ok[ui] = true;
@@ -2446,7 +2469,7 @@ int lsg_solver_launches_per_step(const lsg_solver* s, int* n) {
         if (!s || !n) fail(LSG_EINVAL, "launches_per_step: null argument");
         int per_stage = 0;  // one launch, or boundary bands + interior (run_stage)
         for (const Slab& sl : s->slabs)
-            per_stage += s->halo_w == 0 ? 1 : (sl.nz > 2 * s->halo_w ? 2 : 1);
+            per_stage += (s->halo_w == 0 || !s->overlap_halo) ? 1 : (sl.nz > 2 * s->halo_w ? 2 : 1);
         *n = stages_of(s->method) * per_stage;
     });
 }

@@ -33,8 +33,10 @@ def dctx():
     c.close()
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("name", ["cfg2", "cfg1", "cfg3", "cfg4", "cfg5", "rockets"])
-def test_dist_branch_equals_single_device(ctx, dctx, port, name):
+def test_dist_branch_equals_single_device(ctx, dctx, port, monkeypatch, name, overlap):
+    monkeypatch.setenv("LSG_HALO_OVERLAP", overlap)
     S = P.CONFIGS[name](**H.small(name))
     v0 = H.initial_value(port, S)
     one = _lib.Solver(ctx, S.grid, S.problem, S.method)

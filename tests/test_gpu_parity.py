@@ -224,13 +224,16 @@ def test_cfg1_full_size_vs_golden(ctx, port, sums):
     assert sha(v) == e["out"] and len(steps) == e["n_steps"] == 118
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("name,nslabs", [("cfg2", 2), ("cfg2", 3), ("cfg5", 4), ("cfg3", 2), ("cfg1", 5),
                                          ("cfg4", 2), ("cfg2", 4), ("cfg3", 3), ("rotation", 7)])
-def test_slabs_equal_single_device_bitwise(ctx, port, name, nslabs):
+def test_slabs_equal_single_device_bitwise(ctx, port, monkeypatch, name, nslabs, overlap):
     """P slabs along the last axis == the single-slab result, bit for bit,
-    including the step log.  Ghost planes move on a second stream while the
-    interior planes are computed; thin slabs (nz <= 2W) take the
-    boundary-only path."""
+    including the step log, in both halo modes: overlapped (ghost planes move
+    on a second stream while the interior planes are computed; thin slabs
+    (nz <= 2W) take the boundary-only path) and exchange-then-stage (the
+    large-slab mode)."""
+    monkeypatch.setenv("LSG_HALO_OVERLAP", overlap)
     S = P.CONFIGS[name](**H.small(name))
     v0 = H.initial_value(port, S)
     one = _lib.Solver(ctx, S.grid, S.problem, S.method)
@@ -530,11 +533,13 @@ def test_integrate_5d_6d_all_schemes(ctx, port, D, scheme):
         assert_bitwise(va, vb, f"v D={D} s={scheme}")
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("nslabs", [1, 2, 7])
-def test_launches_per_step_matches_counted_launches(ctx, nslabs):
+def test_launches_per_step_matches_counted_launches(ctx, monkeypatch, nslabs, overlap):
     """lsg_solver_launches_per_step equals the kernels a step actually launches
     (one per stage, or boundary bands + interior per slab; thin slabs one)."""
     import ctypes as C
+    monkeypatch.setenv("LSG_HALO_OVERLAP", overlap)
     S = P.cfg2_air3d(21)
     s = _lib.Solver(ctx, S.grid, S.problem, S.method, nslabs=nslabs)
     s.init_shape(*S.ic[:3], S.ic[3])
