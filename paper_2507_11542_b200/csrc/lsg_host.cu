@@ -544,11 +544,6 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     s->total = node_count(g);
     for (int d = 0; d + 1 < s->D; ++d) s->plane *= g->counts[d];
     s->halo_w = (s->P > 1 || s->distributed) ? s->W : 0;
-    {
-        const long long slab_nodes = s->total / std::max(1, s->P);
-        s->overlap_halo = slab_nodes < (32LL << 20);  // 32 Mi nodes: ~0.4-4 ms stages vs ~20-40 us exchanges
-        if (const char* e = std::getenv("LSG_HALO_OVERLAP")) s->overlap_halo = std::string(e) != "0";
-    }
     if (s->halo_w) {
         // halo traffic and boundary bands sit on the critical path of the next
         // stage: their blocks go ahead of the interior's when SMs free up
@@ -720,6 +715,15 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                 for (auto& fm : s->m3fn) fm[0] = fm[1] = nullptr;
             }
         }
+    }
+
+    // halo mode: large slabs of the tiled 3-D kernels exchange before each
+    // stage's single launch (the band launch of a many-tile grid costs more
+    // than the ~20-40 us exchange it would hide); everything else overlaps
+    {
+        const long long slab_nodes = s->total / std::max(1, s->P);
+        s->overlap_halo = !(s->m3fn[0][0] && slab_nodes >= (32LL << 20));
+        if (const char* e = std::getenv("LSG_HALO_OVERLAP")) s->overlap_halo = std::string(e) != "0";
     }
 
     // slabs
