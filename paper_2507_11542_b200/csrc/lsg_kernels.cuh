@@ -88,7 +88,8 @@ __device__ __forceinline__ double stage_node(const StageParams& P, const double*
 #pragma unroll
     for (int d = 0; d < D; ++d) {
         double s[2 * W + 1];
-        gather_window<W>(u, idx, i[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s);
+        gather_window<W>(u, idx, i[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s,
+                         -(long long)P.halo * W * P.plane, P.n_local + (long long)P.halo * W * P.plane);
         double L, R;
         line_lr<S>(s, P.lc[d], L, R);
         p[d] = 0.5 * (L + R);              // hamiltonian.cpp:31-32

@@ -162,6 +162,8 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
     const long long s2 = P.stride[2];
     const double* cur = zpl[W] - me;
     const int idx = coli + z * (int)s2;
+    LSG_CHECK(idx >= 0 && idx + (two ? 1 : 0) < P.n_local);
+    LSG_CHECK(me - W * pitch - W - SH >= 0);
     double L, R;
     double pa[3], pb[3];
     double da = 0.0, db = 0.0;
@@ -574,6 +576,16 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
         border || (P.bc[2] != LSG_BC_PERIODIC && (P.z0 + zs - W < 0 || P.z0 + ze + W + D > nglob));
     const int nyh = 2 * W * cols, nh = nyh + 2 * W * rows;
 
+#ifdef LSG_CHECKED
+    {
+        unsigned dyn = 0;
+        asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        LSG_CHECK((smem_u32(ring) & 127u) == 0u);
+        LSG_CHECK(reinterpret_cast<const char*>(bar + NB) <= reinterpret_cast<const char*>(sm) + dyn);
+        LSG_CHECK(!active || (me + 1 + W * pitch < slot && vme + 1 < M.vslot));  // padding threads never read
+        LSG_CHECK((me - W - SH) % 2 == 0);
+    }
+#endif
     if (t == 0) {
         for (int j = 0; j < NB; ++j) mbar_init(bar + j, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -613,10 +625,12 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
         if (!border || h >= nh || !halo_cell(h, off, gx, gy)) continue;
         c_off[q] = off;
         const bool wx = gx < 0 || gx >= n0;
+        LSG_CHECK(off >= 0 && off < slot && h < M.hmax);
         if (wx ? P.bc[0] == LSG_BC_PERIODIC : P.bc[1] == LSG_BC_PERIODIC) {
             gx = gx < 0 ? gx + n0 : (gx >= n0 ? gx - n0 : gx);
             gy = gy < 0 ? gy + n1 : (gy >= n1 ? gy - n1 : gy);
             c_a[q] = gy * n0 + gx;
+            LSG_CHECK(c_a[q] >= 0 && c_a[q] < n0 * n1);
         } else if (wx) {
             c_a[q] = off + ((gx < 0 ? 0 : n0 - 1) - gx);
             c_b[q] = (off + ((gx < 0 ? 1 : n0 - 2) - gx)) | ((gx < 0 ? -gx : gx - (n0 - 1)) << 24);
@@ -637,6 +651,9 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
             const int pv = p - W;
             const bool want_v = MODE == MODE_COMBINE && pv >= zs && pv < ze;
             const bool tma_u = want_u && !ghost_plane;
+            LSG_CHECK(j >= 0 && j < NB && vj >= 0 && vj < NV && sj >= 0 && sj < NS);
+            LSG_CHECK(!tma_u || (src + P.halo * W >= 0 && src + P.halo * W < P.n[2] + 2 * P.halo * W));
+            LSG_CHECK(!want_v || (pv >= 0 && pv < P.n[2]));
             mbar_arrive_expect_tx(bar + j, (tma_u ? static_cast<unsigned>(pitch * (M.R + 2 * W) * 8) : 0u) +
                                                (want_v ? static_cast<unsigned>(TX * M.R * 8) : 0u));
             if (tma_u) tma_load_3d(ring + j * slot, &tmu, bar + j, x0 - XL, y0 - W, src + P.halo * W);
@@ -650,6 +667,8 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
             const double k = (double)(zg < 0 ? -zg : zg - (nglob - 1));
             const double* b0 = P.u + (long long)(e0 - P.z0) * s2;
             const double* b1 = P.u + (long long)(e1 - P.z0) * s2;
+            LSG_CHECK(e0 - P.z0 >= -P.halo * W && e0 - P.z0 < P.n[2] + P.halo * W);
+            LSG_CHECK(e1 - P.z0 >= -P.halo * W && e1 - P.z0 < P.n[2] + P.halo * W);
             auto ext = [&](int o) {
                 const double lo = __ldg(b0 + o);
                 return lo + k * (lo - __ldg(b1 + o));
@@ -668,6 +687,7 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
         } else if (border) {
             // periodic wraps: cp.async into the staging slot (copied in after the TMA lands)
             const double* base = P.u + (long long)src * s2;
+            LSG_CHECK(src >= -P.halo * W && src < P.n[2] + P.halo * W);
 #pragma unroll
             for (int q = 0; q < kMaxHalo; ++q)
                 if (c_off[q] >= 0 && c_b[q] < 0) cp_async8(stage + sj * M.hmax + t + q * blockDim.x, base + c_a[q]);
