@@ -292,6 +292,15 @@ March3Fn lookup_march3(int kind, int scheme, int mode, bool range) {
     return nullptr;
 }
 
+MarchNFn lookup_marchn(int kind, int D, int scheme, int mode, bool range) {
+    switch (kind) {
+        case LSG_HAM_LINEAR: return marchn_lookup_linear(D, scheme, mode, range);
+        case LSG_HAM_DBLINT4: return marchn_lookup_dblint4(D, scheme, mode, range);
+        case LSG_HAM_DUBINS6: return marchn_lookup_dubins6(D, scheme, mode, range);
+    }
+    return nullptr;
+}
+
 March3TmaFn lookup_march3_tma(int kind, int scheme, int mode, bool range) {
     switch (kind) {
         case LSG_HAM_LINEAR: return march3_tma_lookup_linear(scheme, mode, range);
@@ -471,6 +480,7 @@ struct lsg_solver {
     StageFn fn[3] = {nullptr, nullptr, nullptr};
     March3Fn m3fn[3][2] = {};  // [mode][with v-range reduction]
     March3TmaFn m3tfn[3][2] = {};  // TMA-fed variant (even rows; LSG_TMA=0 disables)
+    MarchNFn mnfn[3][2] = {};      // 4-D..6-D tile-and-march kernel
     Box3Fn b3fn[3][2] = {};
     int m3_threads = 0;
     int m3_pitch = 0;
@@ -585,7 +595,16 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     // 2.5-D tiled kernel for 3-D grids (lsg_march3.cuh): TX x R tiles, two
     // x-adjacent nodes per thread, 256 threads per block.
     int TX = 0, R = 0;
-    if (s->invalid.empty() && s->D == 3 && !force_generic() && !s->b3fn[0][0]) {
+    // 4-D..6-D grids: the tile-and-march kernel over their first three axes
+    // (lsg_marchn.cuh, same tile shapes) where it measured faster than the
+    // one-node-per-thread kernel — the fast WENO5 in 4-D (cfg3 81^4: 30.4 ->
+    // 33.5 G); elsewhere the generic kernel's 4 blocks per SM win (cfg3 exact
+    // 14.8 vs 14.0 G, cfg4 exact 9.1 vs 7.9 G, ENO3 22.1 vs 19.9 G).
+    // LSG_KERNEL=marchn forces it wherever it is instantiated.
+    const bool marchn_ok = s->invalid.empty() && s->D >= 4 && !force_generic() && !kernel_choice("box3") &&
+                           lookup_marchn(p->kind, s->D, kscheme, 0, false) != nullptr &&
+                           (kernel_choice("marchn") || (kscheme == WENO5F && s->D == 4));
+    if (s->invalid.empty() && (s->D == 3 || marchn_ok) && !force_generic() && !s->b3fn[0][0]) {
         const int n0 = g->counts[0], n1 = g->counts[1];
         const int W = s->W;
         // tile shapes in order of preference: full rows (no x halo), then x
@@ -658,7 +677,32 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
             }
         }
         const long long padded_nodes = static_cast<long long>(g->counts[2] + 2 * W) * n0 * n1;
-        if (fits && padded_nodes < (1LL << 31) - 1) {
+        if (fits && marchn_ok) {
+            bool all = true;
+            for (int m = 0; m < 3; ++m)
+                for (int r = 0; r < 2; ++r) {
+                    s->mnfn[m][r] = lookup_marchn(p->kind, s->D, kscheme, m, r == 1);
+                    all = all && s->mnfn[m][r];
+                }
+            if (all) {
+                s->m3_threads = threads;
+                const int Wr = s->W, SHr = Wr & 1, XWr = (2 * Wr + 2 + SHr + 1) & ~1;
+                s->m3_pitch = (TX + XWr - 2 + 1) & ~1;
+                const int NB = 2 * Wr + 1 + 2, NV = 3;  // RingShape<W>
+                s->m3_smem = sizeof(double) * static_cast<size_t>(NB * s->m3_pitch * (R + 2 * Wr) + NV * TX * R);
+                for (int m = 0; m < 3; ++m)
+                    for (int r = 0; r < 2; ++r)
+                        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->mnfn[m][r]),
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        static_cast<int>(s->m3_smem)));
+                int per_sm = 0;
+                CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &per_sm, reinterpret_cast<const void*>(s->mnfn[2][1]), threads, s->m3_smem));
+                s->m3_per_sm = std::max(1, per_sm);
+            } else {
+                for (auto& fm : s->mnfn) fm[0] = fm[1] = nullptr;
+            }
+        } else if (fits && s->D == 3 && padded_nodes < (1LL << 31) - 1) {
             bool all = true;
             for (int m = 0; m < 3; ++m)
                 for (int r = 0; r < 2; ++r) {
@@ -722,7 +766,7 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
     // than the ~20-40 us exchange it would hide); everything else overlaps
     {
         const long long slab_nodes = s->total / std::max(1, s->P);
-        s->overlap_halo = !(s->m3fn[0][0] && slab_nodes >= (32LL << 20));
+        s->overlap_halo = !((s->m3fn[0][0] || s->mnfn[0][0]) && slab_nodes >= (32LL << 20));
         if (const char* e = std::getenv("LSG_HALO_OVERLAP")) s->overlap_halo = std::string(e) != "0";
     }
 
@@ -736,6 +780,25 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
         if (s->P > 1 && sl.nz < s->W)
             fail(LSG_EINVAL, "slab decomposition: each slab needs at least " + std::to_string(s->W) + " planes");
         sl.nodes = static_cast<long long>(sl.nz) * s->plane;
+        if (s->mnfn[0][0]) {
+            // tiles x outer indices x z-chunks of axis 2: enough blocks for >= 4 waves
+            const int ntx = (g->counts[0] + TX - 1) / TX, nty = (g->counts[1] + R - 1) / R;
+            long long outer = sl.nz;
+            for (int d = 3; d + 1 < s->D; ++d) outer *= g->counts[d];
+            const long long blocks = static_cast<long long>(ntx) * nty * outer;
+            const long long want = 4LL * 148 * s->m3_per_sm;
+            int nzc = static_cast<int>(std::min<long long>(std::max<long long>(1, (want + blocks - 1) / blocks),
+                                                           std::max(1, g->counts[2] / 8)));
+            if (const char* e = std::getenv("LSG_M3_CHUNK")) {
+                const int chunk = std::max(1, std::min(g->counts[2], std::atoi(e)));
+                nzc = (g->counts[2] + chunk - 1) / chunk;
+            }
+            if (std::getenv("LSG_M3_VERBOSE"))
+                std::fprintf(stderr, "marchn D=%d: TX=%d R=%d tiles=%d outer=%lld chunks=%d blocks/SM=%d smem=%zu\n",
+                             s->D, TX, R, ntx * nty, outer, nzc, s->m3_per_sm, s->m3_smem);
+            sl.m3 = March3{TX, R, ntx, nzc, s->m3_pitch, 0, 0, 0};
+            sl.m3_grid = dim3(static_cast<unsigned>(ntx * nty), static_cast<unsigned>(nzc));
+        }
         if (s->m3fn[0][0]) {
             // tiles x z-chunks: minimise waves * (planes per chunk + warm-up) over 148 SMs
             const int ntx = (g->counts[0] + TX - 1) / TX, nty = (g->counts[1] + R - 1) / R;
@@ -1072,6 +1135,23 @@ void launch_planes(lsg_solver* s, Slab& sl, int mode, int ui, int vi, int oi, do
         CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(s->b3fn[mode][range ? 1 : 0]),
                                     dim3(static_cast<unsigned>((pl + 255) / 256), static_cast<unsigned>(zhi - zlo)),
                                     dim3(256), args, 0, stream));
+    } else if (s->mnfn[mode][0]) {
+        March3 M = sl.m3;
+        long long mid = 1;
+        for (int d = 3; d + 1 < s->D; ++d) mid *= s->g.counts[d];
+        const long long gx = static_cast<long long>(sl.m3_grid.x) * mid * (zhi - zlo);
+        void* args[] = {&P, &M};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(M.nzc));
+        cfg.blockDim = dim3(static_cast<unsigned>(s->m3_threads));
+        cfg.dynamicSmemBytes = s->m3_smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = s->pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_CHECK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(s->mnfn[mode][range ? 1 : 0]), args));
     } else if (s->m3fn[mode][0]) {
         March3 M = sl.m3;
         if (zhi - zlo < sl.nz)  // a partial range: chunks of >= 3 planes

@@ -5,6 +5,7 @@
 
 #include "lsg_box3.cuh"
 #include "lsg_march3.cuh"
+#include "lsg_marchn.cuh"
 
 namespace lsg {
 
@@ -34,6 +35,9 @@ March3Fn march3_lookup_normal(int s, int m, bool range);
 March3Fn march3_lookup_rockets(int s, int m, bool range);
 March3Fn march3_lookup_air3d(int s, int m, bool range);
 March3TmaFn march3_tma_lookup_linear(int s, int m, bool range);
+MarchNFn marchn_lookup_linear(int D, int s, int m, bool range);
+MarchNFn marchn_lookup_dblint4(int D, int s, int m, bool range);
+MarchNFn marchn_lookup_dubins6(int D, int s, int m, bool range);
 March3TmaFn march3_tma_lookup_normal(int s, int m, bool range);
 March3TmaFn march3_tma_lookup_rockets(int s, int m, bool range);
 March3TmaFn march3_tma_lookup_air3d(int s, int m, bool range);

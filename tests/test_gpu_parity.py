@@ -760,3 +760,30 @@ def test_cfg4_full_size_slabs_step_log(ctx):
     assert_bitwise(out[0][0], out[1][0], "step log at 41^6, 1 vs 3 slabs")
     assert out[0][1] == out[1][1]
     assert np.all(np.isfinite(out[0][0]))
+
+
+@pytest.mark.parametrize("dims,periodic", [((9, 8, 7, 8), ()), ((9, 8, 7, 10), (1, 3)), ((8, 7, 7, 7, 7, 8), (2, 5)),
+                                           ((7, 9, 7, 7, 7, 7), (0, 1, 2, 3, 4, 5))])
+@pytest.mark.parametrize("nslabs", [1, 2])
+def test_marchn_kernel_vs_oracle(ctx, port, monkeypatch, dims, periodic, nslabs):
+    """LSG_KERNEL=marchn: the 4-D/6-D tile-and-march kernel (lsg_marchn.cuh) for
+    every scheme, both clamps, slabs, bit for bit against the oracle (linear
+    Hamiltonian in 4-D, the cfg4 Dubins Hamiltonian in 6-D)."""
+    monkeypatch.setenv("LSG_KERNEL", "marchn")
+    D = len(dims)
+    g = abi.make_grid([-1.0] * D, [1.0] * D, list(dims), periodic)
+    v = H.random_field(g, sum(dims) + nslabs)
+    for s in range(4):
+        if D == 4:
+            p = abi.make_problem(abi.HAM_LINEAR, s, abi.linear_params([0.7, -1.1, 0.4, 0.9]), abi.GROW, s % 2 == 1)
+        else:
+            p = abi.make_problem(abi.HAM_DUBINS6, s, [], abi.GROW, s % 2 == 1)
+        sol = _lib.Solver(ctx, g, p, abi.CFL3, nslabs=nslabs)
+        sol.set_field(v)
+        tf = 2.5 * 0.32 * sol.step_bound()
+        sa, _ = sol.integrate(0.0, tf)
+        va = sol.get_field()
+        sol.close()
+        vb, sb, _ = port.integrate(g, p, abi.CFL3, 0.0, tf, v)
+        assert_bitwise(sa, sb, f"steps scheme {s}")
+        assert_bitwise(va, vb, f"v scheme {s}")
