@@ -599,16 +599,23 @@ def b200_arm(args):
     eff = None
     if ws > 1 and scaling == "weak" and not args.no_efficiency:
         if rank == 0:
+            # a plain single-GPU context: the distributed one would make the
+            # solver collective (and wait for the idle ranks)
+            ctx1 = _lib.Context(local)
             S1, c1, _ = workload(args.config, scheme, 1)
-            sol = build(S1)
-            T1 = Timed(torch, ctx, sol, 0.32 * sol.step_bound(), stream, flush)
+            sol = _lib.Solver(ctx1, S1.grid, S1.problem, S1.method)
+            shape, center, radius, ignored = S1.ic
+            sol.init_shape(shape, center, radius, ignored)
+            stream1 = torch.cuda.ExternalStream(sol.stream())
+            T1 = Timed(torch, ctx1, sol, 0.32 * sol.step_bound(), stream1, flush)
             T1.warm(args.warmup)
             ms1, _ = T1.run(args.steps, lambda: torch.cuda.synchronize())
             v1 = c1["nodes"] * stages * args.steps / (ms1 * 1e-3)
             eff = {"value_1gpu_same_run": v1, "weak_scaling_efficiency": value / (ws * v1),
-                   "note": "rank 0 re-runs the N=1 workload after the timed multi-rank region (other ranks idle); "
-                           "the driver's own SCALE efficiency uses the separate N=1 run"}
+                   "note": "rank 0 re-runs the N=1 workload on a single-GPU context after the timed multi-rank "
+                           "region (other ranks idle); the driver's own SCALE efficiency uses the separate N=1 run"}
             sol.close()
+            ctx1.close()
         if dist is not None:
             dist.barrier()
 
