@@ -465,12 +465,25 @@ def b200_arm(args):
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(_lib.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        ctx = _lib.Context(local, rank, ws, bytes(uid.cpu().numpy().tobytes()))
+        # NCCL prints its version banner on stdout at the first communicator
+        # init; keep stdout for the JSON line (the banner and INFO lines go to stderr)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(_lib.nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0)
+            ctx = _lib.Context(local, rank, ws, bytes(uid.cpu().numpy().tobytes()))
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
+        n_comm, r_comm = ctx.comm_info()
+        print(f"bench: rank {rank}: lsg NCCL communicator with {n_comm} ranks (this rank {r_comm})", file=sys.stderr)
     else:
         torch.cuda.set_device(0)
         ctx = _lib.Context(0)
@@ -597,7 +610,7 @@ def b200_arm(args):
 
     # ---- in-run scaling reference (N>1, weak scaling): the 1-GPU workload on rank 0
     eff = None
-    if ws > 1 and scaling == "weak" and not args.no_efficiency:
+    if dist is not None and scaling == "weak" and not args.no_efficiency:  # (also under --dist-selftest)
         if rank == 0:
             # a plain single-GPU context: the distributed one would make the
             # solver collective (and wait for the idle ranks)
