@@ -176,6 +176,13 @@ int lsg_grid_axis(const lsg_grid* g, int d, double* out);
 /* Slab of rank r among P along an axis of n planes: the first n % P ranks
  * hold ceil(n/P) planes, the rest floor(n/P) (host-only, no device needed). */
 int lsg_slab_partition(int n, int nranks, int rank, int* z0, int* nz);
+/* The halo messages a rank issues per exchange, in order (host-only; the
+ * distributed exchange issues exactly these as one NCCL group): kinds[i] 0 =
+ * send, 1 = recv; peers[i] the other rank; planes[i] the first plane relative
+ * to the slab's plane 0 (ghost planes are < 0 or >= its plane count);
+ * counts[i] planes.  At most 4 messages (arrays of 4). */
+int lsg_halo_plan(int n, int nranks, int rank, int width, int periodic, int* kinds, int* peers, int* planes,
+                  int* counts, int* n_messages);
 
 /* ---- stateless reference-facing calls (host buffers in and out) ------------
  * Each call copies its host inputs to the device, runs the kernels, and copies

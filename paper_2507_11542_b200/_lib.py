@@ -37,7 +37,7 @@ EXPORTS = (
     "lsg_solver_step_host",
     "lsg_solver_step_timed",
     "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
-    "lsg_probe_fp64_rate", "lsg_ctx_comm_info", "lsg_gather_field",
+    "lsg_probe_fp64_rate", "lsg_ctx_comm_info", "lsg_gather_field", "lsg_halo_plan",
 )
 
 _lib = None
@@ -489,6 +489,16 @@ def slab_partition(n, nranks, rank):
     z0, nz = C.c_int(), C.c_int()
     call("lsg_slab_partition", C.c_int(n), C.c_int(nranks), C.c_int(rank), C.byref(z0), C.byref(nz))
     return z0.value, nz.value
+
+
+def halo_plan(n, nranks, rank, width, periodic):
+    """The halo messages of rank's exchange in issue order (lsg_halo_plan,
+    host-only): list of (kind 'send'|'recv', peer, first plane, planes)."""
+    k, p, pl, c = (C.c_int * 4)(), (C.c_int * 4)(), (C.c_int * 4)(), (C.c_int * 4)()
+    m = C.c_int()
+    call("lsg_halo_plan", C.c_int(n), C.c_int(nranks), C.c_int(rank), C.c_int(width), C.c_int(1 if periodic else 0),
+         k, p, pl, c, C.byref(m))
+    return [("send" if k[i] == 0 else "recv", p[i], pl[i], c[i]) for i in range(m.value)]
 
 
 def device_count():

@@ -1027,6 +1027,29 @@ void check_alpha_valid(lsg_solver* s) {
         fail(LSG_ENUMERIC, "term_lax_friedrichs: dissipation bound must be finite and non-negative");
 }
 
+// The halo messages of one rank, in issue order (lsg_halo_plan): every rank
+// sends its top W planes up, then its bottom W planes down, then receives the
+// lower ghost planes from below and the upper ones from above, so per peer
+// pair the messages match in issue order even for a 2-rank periodic ring.
+struct HaloMsg {
+    int kind;  // 0 send, 1 recv
+    int peer;
+    int plane;  // first plane, relative to the slab's plane 0 (ghost planes negative / >= nz)
+    int count;  // planes
+};
+int halo_plan(int n, int nranks, int rank, int w, bool periodic, HaloMsg* out) {
+    int z0 = 0, nz = 0;
+    partition(n, nranks, rank, &z0, &nz);
+    const int lo = rank > 0 ? rank - 1 : (periodic ? nranks - 1 : -1);
+    const int hi = rank < nranks - 1 ? rank + 1 : (periodic ? 0 : -1);
+    int k = 0;
+    if (hi >= 0) out[k++] = {0, hi, nz - w, w};
+    if (lo >= 0) out[k++] = {0, lo, 0, w};
+    if (lo >= 0) out[k++] = {1, lo, -w, w};
+    if (hi >= 0) out[k++] = {1, hi, nz, w};
+    return k;
+}
+
 // Fill the ghost planes of buffer b: from the neighbour slabs (device copies
 // in-process, NCCL send/recv across ranks); ring for a periodic last axis.
 void exchange(lsg_solver* s, int b, cudaStream_t st) {
@@ -1054,18 +1077,18 @@ void exchange(lsg_solver* s, int b, cudaStream_t st) {
         }
         return;
     }
-    const int P = ctx->nranks, r = ctx->rank;
-    const int lo = r > 0 ? r - 1 : (periodic ? P - 1 : -1);
-    const int hi = r < P - 1 ? r + 1 : (periodic ? 0 : -1);
     Slab& me = s->slabs[0];
-    const size_t cnt = static_cast<size_t>(w * s->plane);
-    // Per peer pair the messages match in issue order: every rank first sends
-    // up, then down, and receives from below before from above.
+    HaloMsg msg[4];
+    const int nmsg = halo_plan(s->g.counts[s->D - 1], ctx->nranks, ctx->rank, static_cast<int>(w), periodic, msg);
     NCCL_CHECK(ncclGroupStart());
-    if (hi >= 0) NCCL_CHECK(ncclSend(me.f[b] + (me.nz - w) * s->plane, cnt, ncclFloat64, hi, ctx->comm, st));
-    if (lo >= 0) NCCL_CHECK(ncclSend(me.f[b], cnt, ncclFloat64, lo, ctx->comm, st));
-    if (lo >= 0) NCCL_CHECK(ncclRecv(me.f[b] - w * s->plane, cnt, ncclFloat64, lo, ctx->comm, st));
-    if (hi >= 0) NCCL_CHECK(ncclRecv(me.f[b] + me.nz * s->plane, cnt, ncclFloat64, hi, ctx->comm, st));
+    for (int k = 0; k < nmsg; ++k) {
+        double* p = me.f[b] + static_cast<long long>(msg[k].plane) * s->plane;
+        const size_t cnt = static_cast<size_t>(msg[k].count) * static_cast<size_t>(s->plane);
+        if (msg[k].kind == 0)
+            NCCL_CHECK(ncclSend(p, cnt, ncclFloat64, msg[k].peer, ctx->comm, st));
+        else
+            NCCL_CHECK(ncclRecv(p, cnt, ncclFloat64, msg[k].peer, ctx->comm, st));
+    }
     NCCL_CHECK(ncclGroupEnd());
 }
 
@@ -1809,6 +1832,24 @@ int lsg_grid_axis(const lsg_grid* g, int d, double* out) {
         if (d < 0 || d >= g->dim) fail(LSG_EINVAL, "grid: dimension out of range");
         const double dx = spacing(g, d);
         for (int i = 0; i < g->counts[d]; ++i) out[i] = g->mins[d] + static_cast<double>(i) * dx;
+    });
+}
+
+int lsg_halo_plan(int n, int nranks, int rank, int width, int periodic, int* kinds, int* peers, int* planes,
+                  int* counts, int* n_messages) {
+    return guarded([&] {
+        if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks || width < 0)
+            fail(LSG_EINVAL, "halo_plan: invalid arguments");
+        if (!kinds || !peers || !planes || !counts || !n_messages) fail(LSG_EINVAL, "halo_plan: null output");
+        HaloMsg msg[4];
+        const int k = halo_plan(n, nranks, rank, width, periodic != 0, msg);
+        for (int i = 0; i < k; ++i) {
+            kinds[i] = msg[i].kind;
+            peers[i] = msg[i].peer;
+            planes[i] = msg[i].plane;
+            counts[i] = msg[i].count;
+        }
+        *n_messages = k;
     });
 }
 

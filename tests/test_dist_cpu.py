@@ -3,8 +3,9 @@ slab decomposition the multi-GPU path uses.
 
 Each rank takes its slab of the last axis with the product's own partition
 rule (lsg_slab_partition, host-only), exchanges W ghost planes per stage with
-its neighbours in the product's message order (send up, send down, receive
-from below, receive from above; a ring when the axis is periodic), reduces the
+its neighbours by the product's own halo plan (lsg_halo_plan: the messages
+the NCCL exchange issues, in its order — send up, send down, receive from
+below, receive from above; a ring when the axis is periodic), reduces the
 v range with all_reduce(MIN/MAX), and evaluates each stage with the CPU oracle
 on its halo-padded slab.  The gathered result must equal the single-domain
 oracle integration bit for bit — the same property the device path is held to
@@ -73,27 +74,25 @@ def _worker(rank, world, port, nz, periodic_z, scheme, zero_speed, result_q):
     _, bound = port_.term_lf(g, p, 0.0, v_full)
     dt = 0.32 * bound if np.isfinite(bound) else 0.01
 
-    lo = rank - 1 if rank > 0 else (world - 1 if periodic_z else -1)
-    hi = rank + 1 if rank < world - 1 else (0 if periodic_z else -1)
+    plan = _lib.halo_plan(nz, world, rank, W, periodic_z)  # the product's own message list (lsg_halo_plan)
 
     def exchange(u):
-        """ghost planes below/above u's slab, in the product's message order."""
-        send_up = torch.from_numpy(u[(nzl - W) * plane:].copy())
-        send_dn = torch.from_numpy(u[:W * plane].copy())
-        recv_lo = torch.empty(W * plane, dtype=torch.float64)
-        recv_hi = torch.empty(W * plane, dtype=torch.float64)
+        """ghost planes below/above u's slab: the product's halo plan (the
+        messages the NCCL exchange issues, in its order) over gloo."""
+        ghost = {}
         reqs = []
-        if hi >= 0:
-            reqs.append(dist.isend(send_up, hi))
-        if lo >= 0:
-            reqs.append(dist.isend(send_dn, lo))
-        if lo >= 0:
-            reqs.append(dist.irecv(recv_lo, lo))
-        if hi >= 0:
-            reqs.append(dist.irecv(recv_hi, hi))
+        for kind, peer, first, count in plan:
+            if kind == "send":
+                reqs.append(dist.isend(torch.from_numpy(u[first * plane:(first + count) * plane].copy()), peer))
+            else:
+                buf = torch.empty(count * plane, dtype=torch.float64)
+                ghost[first] = buf
+                reqs.append(dist.irecv(buf, peer))
         for r in reqs:
             r.wait()
-        return (recv_lo.numpy() if lo >= 0 else None), (recv_hi.numpy() if hi >= 0 else None)
+        glo = ghost[-W].numpy() if -W in ghost else None
+        ghi = ghost[nzl].numpy() if nzl in ghost else None
+        return glo, ghi
 
     def stage_term(u):
         glo, ghi = exchange(u)
@@ -238,3 +237,27 @@ def test_snapshot_gather_gloo(world, nz, tmp_path):
                        start_method="spawn")
     wrote, same_file, same_field = q.get(timeout=60)
     assert wrote and same_field and same_file
+
+
+def test_halo_plan():
+    """lsg_halo_plan (the message list the distributed exchange issues): ends
+    of an open axis talk to one neighbour, a periodic axis is a ring, a
+    2-rank ring sends both messages to the same peer in a matching order."""
+    from paper_2507_11542_b200 import _lib
+
+    assert _lib.halo_plan(20, 3, 0, 3, False) == [("send", 1, 4, 3), ("recv", 1, 7, 3)]
+    assert _lib.halo_plan(20, 3, 2, 3, False) == [("send", 1, 0, 3), ("recv", 1, -3, 3)]
+    assert _lib.halo_plan(20, 3, 1, 3, False) == [("send", 2, 4, 3), ("send", 0, 0, 3), ("recv", 0, -3, 3),
+                                                  ("recv", 2, 7, 3)]
+    assert _lib.halo_plan(16, 2, 0, 2, True) == [("send", 1, 6, 2), ("send", 1, 0, 2), ("recv", 1, -2, 2),
+                                                 ("recv", 1, 8, 2)]
+    assert _lib.halo_plan(11, 1, 0, 3, True) == [("send", 0, 8, 3), ("send", 0, 0, 3), ("recv", 0, -3, 3),
+                                                 ("recv", 0, 11, 3)]
+    assert _lib.halo_plan(11, 1, 0, 3, False) == []
+    # every send has a matching receive at the peer, in the same relative order
+    for n, P, per in [(41, 8, True), (41, 8, False), (512 * 8, 8, True), (7, 7, True)]:
+        plans = [_lib.halo_plan(n, P, r, 3, per) for r in range(P)]
+        for r in range(P):
+            for kind, peer, first, count in plans[r]:
+                if kind == "send":
+                    assert any(k == "recv" and q == r and c == count for k, q, _, c in plans[peer])
