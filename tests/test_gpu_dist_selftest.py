@@ -67,3 +67,27 @@ def test_dist_branch_stateless_calls(ctx, dctx, port):
     vb, sb, _ = dctx.integrate(S.grid, S.problem, S.method, 0.0, 0.05, v0)
     assert_bitwise(sa, sb, "steps")
     assert_bitwise(va, vb, "v")
+
+
+def test_dist_branch_snapshot_and_gather(ctx, dctx, port, tmp_path):
+    """The collective snapshot (lsg_solver_write_snapshot on a distributed
+    context: NCCL gather to rank 0, which writes) and lsg_gather_field through
+    the NCCL branch give the single-device file and field byte for byte."""
+    S = P.cfg2_air3d(21)
+    v0 = H.initial_value(port, S)
+    one = _lib.Solver(ctx, S.grid, S.problem, S.method)
+    dist = _lib.Solver(dctx, S.grid, S.problem, S.method)
+    one.set_field(v0)
+    dist.set_field(v0)
+    one.integrate(0.0, 0.03)
+    dist.integrate(0.0, 0.03)
+    a, b = tmp_path / "one.snap", tmp_path / "dist.snap"
+    one.write_snapshot(0.03, a)
+    dist.write_snapshot(0.03, b)
+    assert a.read_bytes() == b.read_bytes()
+    g = dctx.gather_field(S.grid, dist.get_field())
+    assert_bitwise(g, one.get_field(), "gathered field")
+    ck, times, steps, _ = dctx.solve_brt(S.grid, S.problem, v0, (0.0, 0.05), 3, gather=True)
+    ck1, times1, steps1, _ = ctx.solve_brt(S.grid, S.problem, v0, (0.0, 0.05), 3)
+    assert_bitwise(ck, ck1, "gathered checkpoints")
+    assert_bitwise(steps, steps1, "step log")
