@@ -127,3 +127,20 @@ def test_weno5_fast_full_tspan_within_tolerance(ctx, port, name, kw):
     tie = 1e-9 * np.max(np.abs(vb))
     away = np.abs(vb) > tie
     assert np.array_equal(np.sign(va[away]), np.sign(vb[away]))
+
+
+@pytest.mark.parametrize("name,kw", [("cfg2", dict(n=51)), ("cfg3", dict(n=21)), ("cfg4", dict(n=9)),
+                                     ("cfg5", dict(n=32)), ("cfg1", dict(n=101))])
+def test_full_tspan_bitwise_vs_oracle(ctx, port, name, kw):
+    """Every config over its whole tspan (hundreds to thousands of RK steps) at a
+    reduced size, with the bit-exact schemes: the final value function and the
+    whole step log equal the oracle bit for bit (north_star: 'after the final
+    step')."""
+    S = P.CONFIGS[name](**kw)
+    v0 = H.initial_value(port, S)
+    t0, tf = S.tspan
+    va, sa, ta = ctx.integrate(S.grid, S.problem, S.method, 0.0, tf - t0, v0)
+    vb, sb, tb = port.integrate(S.grid, S.problem, S.method, 0.0, tf - t0, v0)
+    assert ta == tb and len(sa) == len(sb) >= 10
+    assert_bitwise(sa, sb, "step log")
+    assert_bitwise(va, vb, "final value function")
