@@ -231,6 +231,19 @@ int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const d
                   int* n_out, lsg_steplog* steps, size_t log_cap, size_t* n_steps,
                   double* integration_seconds);
 
+/* Resume a checkpointed solve_brt (the reference has none): the
+ * field v_k of checkpoint k (e.g. read back with lsg_read_snapshot) at the
+ * integration time t_k where that leg stopped (the snapshot's time when the
+ * leg landed on its checkpoint time, as legs do unless the termination
+ * epsilon stops them short, integrator.cpp:37-40).  Runs legs k+1 ..
+ * n_checkpoints-1 exactly as lsg_solve_brt does; checkpoints receives
+ * (n_checkpoints - k) fields starting with v_k, and the step log and
+ * checkpoints equal those of the uninterrupted solve. */
+int lsg_solve_brt_resume(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const double* v_k, int k, double t_k,
+                         double t_first, double t_second, int n_checkpoints, int method, const lsg_opts* opts,
+                         double* checkpoints, double* checkpoint_times, int* n_out, lsg_steplog* steps,
+                         size_t log_cap, size_t* n_steps, double* integration_seconds);
+
 /* ---- checkpoint output in the reference's snapshot format ----------------
  * snapshot.cpp:69-129: text header "dims/counts/mins/maxs/time" (reals with 17
  * significant digits) + little-endian fp64 payload in column-major order. */

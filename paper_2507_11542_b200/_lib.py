@@ -38,6 +38,7 @@ EXPORTS = (
     "lsg_solver_step_timed",
     "lsg_solver_integrate", "lsg_solver_write_snapshot", "lsg_solver_stream", "lsg_solver_launches_per_step",
     "lsg_probe_fp64_rate", "lsg_ctx_comm_info", "lsg_gather_field", "lsg_halo_plan",
+    "lsg_solve_brt_resume",
 )
 
 _lib = None
@@ -277,6 +278,33 @@ class Context:
             ck = np.stack(full) if self.rank == 0 else None
         return ck, times[:k].copy(), _steps(log, n.value, log_cap), secs.value
 
+
+    def solve_brt_resume(self, g, p, v_k, k, t_k, tspan, n_checkpoints, method=abi.CFL3, opts=None, log_cap=4096):
+        """Continue a solve_brt from checkpoint k (field v_k at integration time
+        t_k): the checkpoints k .. n-1, their times, the remaining step log."""
+        v_k = np.ascontiguousarray(v_k, dtype=np.float64)
+        N = self.local_nodes(g)
+        if v_k.size != N:
+            raise ValueError("solve_brt_resume: field size does not match the (local) node count")
+        m = max(1, n_checkpoints - k)
+        ck = np.empty(m * N, dtype=np.float64)
+        times = np.empty(m, dtype=np.float64)
+        n_out, n, secs = C.c_int(), C.c_size_t(), C.c_double()
+        while True:
+            log = (abi.LsgStepLog * log_cap)()
+            rc = load().lsg_solve_brt_resume(self.h, C.byref(g), C.byref(p), abi.dptr(v_k), C.c_int(k),
+                                             C.c_double(t_k), C.c_double(tspan[0]), C.c_double(tspan[1]),
+                                             C.c_int(n_checkpoints), C.c_int(method),
+                                             C.byref(opts) if opts is not None else None, abi.dptr(ck),
+                                             abi.dptr(times), C.byref(n_out), log, C.c_size_t(log_cap), C.byref(n),
+                                             C.byref(secs))
+            if rc == abi.ERANGE and n.value > log_cap:
+                log_cap = n.value
+                continue
+            raise_for(rc)
+            break
+        j = n_out.value
+        return ck[: j * N].reshape(j, N), times[:j].copy(), _steps(log, n.value, log_cap), secs.value
 
     def extract_zero_set_2d(self, g, field):
         """Marching-squares zero contour (contour.cpp:27-97): array (n, 4) of ax, ay, bx, by."""

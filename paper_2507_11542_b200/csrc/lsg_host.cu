@@ -2204,59 +2204,95 @@ int lsg_integrate(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, int met
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// solve_brt (reachability.cpp:135-174) from checkpoint k_start: the field
+// v_start at integration time t_start; legs k_start+1 .. n_checkpoints-1 run
+// as the reference's (equal durations from 0, each leg starting where the
+// previous one stopped), checkpoints[0] = v_start.  k_start = 0, t_start = 0
+// is the reference's solve_brt; k_start > 0 resumes a checkpointed run (the
+// reference has no resume).
+void solve_brt_from(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const double* v_start, int k_start,
+                    double t_start, double t_first, double t_second, int n_checkpoints, int method,
+                    const lsg_opts* opts, double* checkpoints, double* checkpoint_times, int* n_out,
+                    lsg_steplog* steps, size_t log_cap, size_t* n_steps, double* integration_seconds) {
+    activate(ctx);
+    check_grid(g);
+    // reachability.cpp:138-143
+    if (n_checkpoints < 1) fail(LSG_EINVAL, "solve_brt: need at least one checkpoint");
+    if (!std::isfinite(t_first) || !std::isfinite(t_second)) fail(LSG_EINVAL, "solve_brt: tspan must be finite");
+    if (k_start < 0 || k_start >= n_checkpoints) fail(LSG_EINVAL, "solve_brt: resume checkpoint out of range");
+    if (!std::isfinite(t_start)) fail(LSG_EINVAL, "solve_brt: resume time must be finite");
+    long long N = node_count(g);
+    if (ctx->nranks > 1) {  // distributed context: v0 and the checkpoints are this rank's slab
+        int z0 = 0, nz = 0;
+        partition(g->counts[g->dim - 1], ctx->nranks, ctx->rank, &z0, &nz);
+        N = N / g->counts[g->dim - 1] * nz;
+    }
+    const double duration = std::abs(t_second - t_first);
+    const int segments = n_checkpoints - 1;
+    std::memcpy(checkpoints, v_start, sizeof(double) * N);
+    checkpoint_times[0] = k_start == 0 ? 0.0
+                                       : duration * static_cast<double>(k_start) / static_cast<double>(segments);
+    *n_out = 1;
+    if (n_steps) *n_steps = 0;
+    if (integration_seconds) *integration_seconds = 0.0;
+    if (duration == 0.0 || n_checkpoints == 1 || k_start == segments) return;
+    lsg_solver* s = cached_solver(ctx, g, p, method);
+    CallCache call_cache{ctx};
+    // every leg's schedule up front (reachability.cpp:160-170: the next leg
+    // starts from leg.t), so the log capacity is known before device work
+    std::vector<LegPlan> plans;
+    size_t total = 0;
+    double t = t_start;
+    for (int k = k_start + 1; k <= segments; ++k) {
+        const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
+        plans.push_back(plan_leg(s, t, t_end, opts));
+        t = plans.back().t_final;
+        total += plans.back().log.size();
+        if (plans.back().collapsed || plans.back().bound_invalid) break;
+    }
+    check_log_room(total, steps, log_cap, n_steps);
+    upload(s, v_start, 0);
+    std::vector<lsg_steplog> all;
+    const auto start = std::chrono::steady_clock::now();
+    for (int i = 0; i < static_cast<int>(plans.size()); ++i) {
+        const int k = k_start + 1 + i;
+        const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
+        run_leg(s, plans[i]);
+        all.insert(all.end(), plans[i].log.begin(), plans[i].log.end());
+        download(s, checkpoints + static_cast<long long>(i + 1) * N, s->cur);
+        checkpoint_times[i + 1] = t_end;
+        *n_out = i + 2;
+    }
+    const auto stop = std::chrono::steady_clock::now();
+    if (integration_seconds) *integration_seconds = std::chrono::duration<double>(stop - start).count();
+    copy_log(all, steps, log_cap, n_steps);
+}
+
+}  // namespace
+
+extern "C" {
+
 int lsg_solve_brt(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const double* v0, double t_first,
                   double t_second, int n_checkpoints, int method, const lsg_opts* opts, double* checkpoints,
                   double* checkpoint_times, int* n_out, lsg_steplog* steps, size_t log_cap, size_t* n_steps,
                   double* integration_seconds) {
     return guarded([&] {
-        activate(ctx);
-        check_grid(g);
-        // reachability.cpp:138-143
-        if (n_checkpoints < 1) fail(LSG_EINVAL, "solve_brt: need at least one checkpoint");
-        if (!std::isfinite(t_first) || !std::isfinite(t_second)) fail(LSG_EINVAL, "solve_brt: tspan must be finite");
-        long long N = node_count(g);
-        if (ctx->nranks > 1) {  // distributed context: v0 and the checkpoints are this rank's slab
-            int z0 = 0, nz = 0;
-            partition(g->counts[g->dim - 1], ctx->nranks, ctx->rank, &z0, &nz);
-            N = N / g->counts[g->dim - 1] * nz;
-        }
-        const double duration = std::abs(t_second - t_first);
-        std::memcpy(checkpoints, v0, sizeof(double) * N);
-        checkpoint_times[0] = 0.0;
-        *n_out = 1;
-        if (n_steps) *n_steps = 0;
-        if (integration_seconds) *integration_seconds = 0.0;
-        if (duration == 0.0 || n_checkpoints == 1) return;
-        lsg_solver* s = cached_solver(ctx, g, p, method);
-        CallCache call_cache{ctx};
-        const int segments = n_checkpoints - 1;
-        // every leg's schedule up front (reachability.cpp:160-170: the next leg
-        // starts from leg.t), so the log capacity is known before device work
-        std::vector<LegPlan> plans;
-        size_t total = 0;
-        double t = 0.0;
-        for (int k = 1; k <= segments; ++k) {
-            const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
-            plans.push_back(plan_leg(s, t, t_end, opts));
-            t = plans.back().t_final;
-            total += plans.back().log.size();
-            if (plans.back().collapsed || plans.back().bound_invalid) break;
-        }
-        check_log_room(total, steps, log_cap, n_steps);
-        upload(s, v0, 0);
-        std::vector<lsg_steplog> all;
-        const auto start = std::chrono::steady_clock::now();
-        for (int k = 1; k <= static_cast<int>(plans.size()); ++k) {
-            const double t_end = duration * static_cast<double>(k) / static_cast<double>(segments);
-            run_leg(s, plans[k - 1]);
-            all.insert(all.end(), plans[k - 1].log.begin(), plans[k - 1].log.end());
-            download(s, checkpoints + static_cast<long long>(k) * N, s->cur);
-            checkpoint_times[k] = t_end;
-            *n_out = k + 1;
-        }
-        const auto stop = std::chrono::steady_clock::now();
-        if (integration_seconds) *integration_seconds = std::chrono::duration<double>(stop - start).count();
-        copy_log(all, steps, log_cap, n_steps);
+        solve_brt_from(ctx, g, p, v0, 0, 0.0, t_first, t_second, n_checkpoints, method, opts, checkpoints,
+                       checkpoint_times, n_out, steps, log_cap, n_steps, integration_seconds);
+    });
+}
+
+int lsg_solve_brt_resume(lsg_ctx* ctx, const lsg_grid* g, const lsg_problem* p, const double* v_k, int k,
+                         double t_k, double t_first, double t_second, int n_checkpoints, int method,
+                         const lsg_opts* opts, double* checkpoints, double* checkpoint_times, int* n_out,
+                         lsg_steplog* steps, size_t log_cap, size_t* n_steps, double* integration_seconds) {
+    return guarded([&] {
+        solve_brt_from(ctx, g, p, v_k, k, t_k, t_first, t_second, n_checkpoints, method, opts, checkpoints,
+                       checkpoint_times, n_out, steps, log_cap, n_steps, integration_seconds);
     });
 }
 

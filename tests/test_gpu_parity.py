@@ -787,3 +787,27 @@ def test_marchn_kernel_vs_oracle(ctx, port, monkeypatch, dims, periodic, nslabs)
         vb, sb, _ = port.integrate(g, p, abi.CFL3, 0.0, tf, v)
         assert_bitwise(sa, sb, f"steps scheme {s}")
         assert_bitwise(va, vb, f"v scheme {s}")
+
+
+def test_solve_brt_resume_from_snapshot(ctx, port, tmp_path):
+    """A checkpointed solve_brt resumed from its checkpoint-5 snapshot file
+    (reference format, snapshot.cpp:68-129) reproduces the uninterrupted run's
+    later checkpoints and step log bit for bit (resume: SURVEY §5)."""
+    S = P.rockets(20)
+    v0 = port.rocket_initial(20) if hasattr(port, "rocket_initial") else None
+    if v0 is None:
+        s = _lib.Solver(ctx, S.grid, S.problem, S.method)
+        s.init_shape(*S.ic[:3], S.ic[3])
+        v0 = s.get_field()
+        s.close()
+    ck, times, steps, _ = ctx.solve_brt(S.grid, S.problem, v0, S.tspan, S.n_checkpoints)
+    k = 5
+    path = tmp_path / "ck5.snap"
+    _lib.write_snapshot(S.grid, ck[k], times[k], path)
+    g2, vk, tk = _lib.read_snapshot(path)
+    assert tk == times[k]
+    rk, rtimes, rsteps, _ = ctx.solve_brt_resume(S.grid, S.problem, vk, k, tk, S.tspan, S.n_checkpoints)
+    assert_bitwise(rk, ck[k:], "checkpoints k..n-1")
+    assert_bitwise(rtimes, times[k:], "checkpoint times")
+    first = int(np.searchsorted(steps[:, 0], tk))
+    assert_bitwise(rsteps, steps[first:], "remaining step log")
