@@ -6,3 +6,4 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
 python bench.py --impl reference > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err; echo "ref rc=$?"
 bash tools/ncu_bench.sh ${TAG}
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --dist-selftest --steps 20 --no-cpu-baseline > gpurun_out/${TAG}_selftest.json 2> gpurun_out/${TAG}_selftest.err; echo "selftest rc=$?"
