@@ -44,14 +44,11 @@ __global__ void __launch_bounds__(256) box3_kernel(const __grid_constant__ Stage
         double p[3];
         double diss = 0.0, L, R;
         line_lr<S>(w0, P.lc[0], L, R);
-        p[0] = 0.5 * (L + R);
-        diss += P.alpha[0] * (R - L);
+        costate<S>(P, 0, L, R, p[0], diss);
         line_lr<S>(w1, P.lc[1], L, R);
-        p[1] = 0.5 * (L + R);
-        diss += P.alpha[1] * (R - L);
+        costate<S>(P, 1, L, R, p[1], diss);
         line_lr<S>(w2, P.lc[2], L, R);
-        p[2] = 0.5 * (L + R);
-        diss += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, p[2], diss);
         const double xs[3] = {__ldg(P.axis[0] + x), __ldg(P.axis[1] + y), __ldg(P.axis[2] + zg)};
         const double H = hamiltonian<KIND, 3>(P, xs, load_trig<KIND>(P, zg, 0), p);
         bad = !isfinite(H);

@@ -219,6 +219,7 @@ LineConst line_const(const lsg_grid* g, int d) {
     c.half_inv = 0.5 * c.inv_dx;
     c.third_inv = c.inv_dx / 3.0;
     c.dx2 = c.dx * c.dx;
+    c.hs6 = 0.5 * (c.inv_dx * (1.0 / 6.0));
     return c;
 }
 
@@ -1114,6 +1115,7 @@ StageParams slab_params(lsg_solver* s, const Slab& sl) {
         P.bc[d] = bc_of(&s->g, d);
         P.lc[d] = s->lc[d];
         P.alpha[d] = s->alpha[d];
+        P.alpha_f[d] = s->alpha[d] * (s->lc[d].inv_dx * (1.0 / 6.0));
         P.axis[d] = s->axis[d];
         P.tcos[d] = s->tcos[d];
         P.tsin[d] = s->tsin[d];

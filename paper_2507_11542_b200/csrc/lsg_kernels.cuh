@@ -92,8 +92,7 @@ __device__ __forceinline__ double stage_node(const StageParams& P, const double*
                          -(long long)P.halo * W * P.plane, P.n_local + (long long)P.halo * W * P.plane);
         double L, R;
         line_lr<S>(s, P.lc[d], L, R);
-        p[d] = 0.5 * (L + R);              // hamiltonian.cpp:31-32
-        diss += P.alpha[d] * (R - L);       // hamiltonian.cpp:60-64
+        costate<S>(P, d, L, R, p[d], diss);  // hamiltonian.cpp:31-32, 60-64
     }
     const double H = hamiltonian<KIND, D>(P, x, load_trig<KIND>(P, D > 2 ? ix[D > 2 ? 2 : 0] : 0, D > 5 ? ix[D > 5 ? 5 : 0] : 0), p);
     bad |= !isfinite(H);                    // hamiltonian.cpp:38-40

@@ -178,10 +178,8 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
         }
         double L2, R2;
         line_lr2<S>(wx + SH, P.lc[0], L, R, L2, R2);
-        pa[0] = 0.5 * (L + R);
-        da += P.alpha[0] * (R - L);
-        pb[0] = 0.5 * (L2 + R2);
-        db += P.alpha[0] * (R2 - L2);
+        costate<S>(P, 0, L, R, pa[0], da);
+        costate<S>(P, 0, L2, R2, pb[0], db);
     }
     double ca, cb;  // centre values
     {   // y: one 128-bit load per row gives both nodes' windows
@@ -195,20 +193,16 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
         ca = wa[W];
         cb = wb[W];
         line_lr<S>(wa, P.lc[1], L, R);
-        pa[1] = 0.5 * (L + R);
-        da += P.alpha[1] * (R - L);
+        costate<S>(P, 1, L, R, pa[1], da);
         line_lr<S>(wb, P.lc[1], L, R);
-        pb[1] = 0.5 * (L + R);
-        db += P.alpha[1] * (R - L);
+        costate<S>(P, 1, L, R, pb[1], db);
     }
     if (ZC && S == ENO3 && !first) {  // z: carried tables + the newest plane
         const double2 v = *reinterpret_cast<const double2*>(zpl[2 * W]);
         eno3_z_step(v.x, P.lc[2], *qa, L, R);
-        pa[2] = 0.5 * (L + R);
-        da += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, pa[2], da);
         eno3_z_step(v.y, P.lc[2], *qb, L, R);
-        pb[2] = 0.5 * (L + R);
-        db += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, pb[2], db);
     } else {   // z: the pair's slot in the 2W+1 resident planes
         double wa[2 * W + 1], wb[2 * W + 1];
 #pragma unroll
@@ -218,11 +212,9 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
             wb[W + k] = v.y;
         }
         line_lr<S>(wa, P.lc[2], L, R);
-        pa[2] = 0.5 * (L + R);
-        da += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, pa[2], da);
         line_lr<S>(wb, P.lc[2], L, R);
-        pb[2] = 0.5 * (L + R);
-        db += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, pb[2], db);
         if constexpr (ZC && S == ENO3) {
             eno3_z_init(wa, P.lc[2], *qa);
             eno3_z_init(wb, P.lc[2], *qb);

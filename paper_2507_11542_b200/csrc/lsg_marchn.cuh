@@ -45,10 +45,8 @@ __device__ __forceinline__ void marchn_pair(const StageParams& P, const double* 
         }
         double L2, R2;
         line_lr2<S>(wx + SH, P.lc[0], L, R, L2, R2);
-        pa[0] = 0.5 * (L + R);
-        da += P.alpha[0] * (R - L);
-        pb[0] = 0.5 * (L2 + R2);
-        db += P.alpha[0] * (R2 - L2);
+        costate<S>(P, 0, L, R, pa[0], da);
+        costate<S>(P, 0, L2, R2, pb[0], db);
     }
     double ca, cb;
     {   // y
@@ -62,11 +60,9 @@ __device__ __forceinline__ void marchn_pair(const StageParams& P, const double* 
         ca = wa[W];
         cb = wb[W];
         line_lr<S>(wa, P.lc[1], L, R);
-        pa[1] = 0.5 * (L + R);
-        da += P.alpha[1] * (R - L);
+        costate<S>(P, 1, L, R, pa[1], da);
         line_lr<S>(wb, P.lc[1], L, R);
-        pb[1] = 0.5 * (L + R);
-        db += P.alpha[1] * (R - L);
+        costate<S>(P, 1, L, R, pb[1], db);
     }
     {   // z
         double wa[2 * W + 1], wb[2 * W + 1];
@@ -77,11 +73,9 @@ __device__ __forceinline__ void marchn_pair(const StageParams& P, const double* 
             wb[W + k] = v.y;
         }
         line_lr<S>(wa, P.lc[2], L, R);
-        pa[2] = 0.5 * (L + R);
-        da += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, pa[2], da);
         line_lr<S>(wb, P.lc[2], L, R);
-        pb[2] = 0.5 * (L + R);
-        db += P.alpha[2] * (R - L);
+        costate<S>(P, 2, L, R, pb[2], db);
     }
     const long long lo = -(long long)P.halo * W * P.plane, hi = P.n_local + (long long)P.halo * W * P.plane;
 #pragma unroll
@@ -90,15 +84,13 @@ __device__ __forceinline__ void marchn_pair(const StageParams& P, const double* 
         gather_window<W>(P.u, idx, io[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s, lo,
                          hi);
         line_lr<S>(s, P.lc[d], L, R);
-        pa[d] = 0.5 * (L + R);
-        da += P.alpha[d] * (R - L);
+        costate<S>(P, d, L, R, pa[d], da);
         if (two) {
             gather_window<W>(P.u, idx + 1, io[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo,
                              s, lo, hi);
             line_lr<S>(s, P.lc[d], L, R);
         }
-        pb[d] = 0.5 * (L + R);
-        db += P.alpha[d] * (R - L);
+        costate<S>(P, d, L, R, pb[d], db);
     }
     double b0 = 0.0, b1 = 0.0;
     if (MODE == MODE_COMBINE) {
