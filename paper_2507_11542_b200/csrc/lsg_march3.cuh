@@ -1,4 +1,8 @@
-// lsg_march3.cuh — 2.5-D tiled fused stage kernel for 3-D grids (sm_100a).
+// lsg_march3.cuh — 2.5-D tiled fused stage kernels for 3-D grids (sm_100a):
+// march3_tma_kernel (rows of an even number of doubles: each plane of a tile
+// arrives by one cp.async.bulk.tensor.3d on an mbarrier ring; see its own
+// comment below) and march3_kernel (any rows: per-thread cp.async), sharing
+// the per-pair arithmetic (march3_pair).  What follows describes both.
 //
 // Block = a TX x R tile of the (x, y) plane (full rows when they fit, else
 // x segments), marching along z through a balanced chunk of planes.  Each
