@@ -17,8 +17,9 @@ import numpy as np
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# LSG_LIB=checked selects the bounds-checked build (make -C csrc checked; tools/checked_run.sh)
-LIB_PATH = os.path.join(HERE, "liblsg_b200_checked.so" if os.environ.get("LSG_LIB") == "checked" else "liblsg_b200.so")
+# LSG_LIB=checked selects the bounds-checked build (make -C csrc checked; tools/checked_run.sh),
+# LSG_LIB=<name> the in-tree liblsg_b200_<name>.so (A/B of two builds on one box)
+LIB_PATH = os.path.join(HERE, "liblsg_b200_%s.so" % os.environ["LSG_LIB"] if os.environ.get("LSG_LIB") else "liblsg_b200.so")
 
 # every symbol include/lsg.h declares
 EXPORTS = (

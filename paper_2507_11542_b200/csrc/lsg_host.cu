@@ -720,11 +720,21 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                             CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->m3fn[m][r]),
                                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                             static_cast<int>(s->m3_smem)));
-                // TMA-fed tiles where rows are 16-byte multiples and the boxes fit
+                // TMA-fed tiles where rows are 16-byte multiples and the boxes fit.
+                // WENO5 runs the y pass (march3_tma_kernel): one item of two rows
+                // per thread, so R is made even (one row less) where needed
                 const char* te = std::getenv("LSG_TMA");
-                const int rows_box = R + 2 * Wr;
-                if (!(te && std::string(te) == "0") && n0 % 2 == 0 && s->m3_pitch <= 256 && rows_box <= 256 &&
-                    TX <= 256 && R <= 256 && encode_tiled()) {
+                const bool yp = kscheme >= WENO5;
+                int Rt = R, tht = threads;
+                if (yp && Rt % 2 == 1 && Rt > 1) {
+                    Rt -= 1;
+                    tht = ((TX / 2 * Rt + 31) / 32) * 32;
+                }
+                const bool yp_ok = !yp || (Rt % 2 == 0 && TX * Rt <= 2 * tht &&
+                                           2 * Wr * std::min(TX, n0) + 2 * Wr * Rt <= kMaxHalo * tht);
+                const int rows_box = Rt + 2 * Wr;
+                if (!(te && std::string(te) == "0") && yp_ok && n0 % 2 == 0 && s->m3_pitch <= 256 &&
+                    rows_box <= 256 && TX <= 256 && Rt <= 256 && encode_tiled()) {
                     bool allt = true;
                     for (int m = 0; m < 3; ++m)
                         for (int r = 0; r < 2; ++r) {
@@ -732,11 +742,15 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                             allt = allt && s->m3tfn[m][r];
                         }
                     if (allt) {
+                        R = Rt;
+                        threads = tht;
+                        s->m3_threads = threads;
                         s->m3_slot = ((s->m3_pitch * rows_box + 15) / 16) * 16;
                         s->m3_vslot = ((TX * R + 15) / 16) * 16;
                         s->m3_hmax = 2 * Wr * (TX + R);
                         s->m3_smem = sizeof(double) * static_cast<size_t>(NB * s->m3_slot + NV * s->m3_vslot +
-                                                                          (2 + 1) * s->m3_hmax) +
+                                                                          (2 + 1) * s->m3_hmax +
+                                                                          (yp ? 4 * TX * R : 0)) +  // y-pass buffers
                                      sizeof(unsigned long long) * NB + 128;  // + alignment slack
                         for (int m = 0; m < 3; ++m)
                             for (int r = 0; r < 2; ++r)

@@ -154,12 +154,14 @@ __device__ __forceinline__ void eno3_z_step(double s6, const LineConst& c, Eno3Z
 // combination, the output store and the step's range candidates.
 // ZC (ENO3 only): z tables carried in qa/qb (first: the chunk's first plane,
 // which fills them from the full window).
-template <int S, int KIND, int MODE, bool RANGE, bool ZC = false>
+// YP: the y-direction costates and dissipation terms of the pair come
+// precomputed (ypr[0], ypr[1]: (p, alpha*(R-L)) per node, the y pass of march3_tma_kernel).
+template <int S, int KIND, int MODE, bool RANGE, bool ZC = false, bool YP = false>
 __device__ __forceinline__ void march3_pair(const StageParams& P, const double* const* zpl, int me, int pitch,
                                             const double* vpair, int coli, int z, bool two, double ax0, double ax1,
                                             double ay, double az, const Trig& tr, unsigned long long& kmin,
                                             unsigned long long& kmax, unsigned& fz, bool& bad, Eno3Z* qa = nullptr,
-                                            Eno3Z* qb = nullptr, bool first = true) {
+                                            Eno3Z* qb = nullptr, bool first = true, const double2* ypr = nullptr) {
     constexpr int W = SchemeWidth<S>::W;
     using RS = RingShape<W>;
     constexpr int SH = RS::SH, XW = RS::XW;
@@ -171,6 +173,7 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
     double L, R;
     double pa[3], pb[3];
     double da = 0.0, db = 0.0;
+    double ca, cb;  // centre values
     {   // x: 2W+2 consecutive padded-line values shared by the pair
         double wx[XW];
         const double* xrow = cur + me - W - SH;
@@ -184,9 +187,16 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
         line_lr2<S>(wx + SH, P.lc[0], L, R, L2, R2);
         costate<S>(P, 0, L, R, pa[0], da);
         costate<S>(P, 0, L2, R2, pb[0], db);
+        ca = wx[W + SH];
+        cb = wx[W + SH + 1];
     }
-    double ca, cb;  // centre values
-    {   // y: one 128-bit load per row gives both nodes' windows
+    if constexpr (YP) {
+        const double2 ya = ypr[0], yb = ypr[1];
+        pa[1] = ya.x;
+        da += ya.y;
+        pb[1] = yb.x;
+        db += yb.y;
+    } else {   // y: one 128-bit load per row gives both nodes' windows
         double wa[2 * W + 1], wb[2 * W + 1];
 #pragma unroll
         for (int k = -W; k <= W; ++k) {
@@ -194,8 +204,6 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
             wa[W + k] = v.x;
             wb[W + k] = v.y;
         }
-        ca = wa[W];
-        cb = wb[W];
         line_lr<S>(wa, P.lc[1], L, R);
         costate<S>(P, 1, L, R, pa[1], da);
         line_lr<S>(wb, P.lc[1], L, R);
@@ -534,6 +542,13 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
     constexpr int D = RS::D, NB = RS::NB, NV = RS::NV, SH = RS::SH;
     constexpr int XL = W + SH;  // box columns start XL left of the tile
     constexpr int NS = D + 1;   // staging slots (planes whose wrap cells are in flight)
+    // y pass (WENO5, both forms): the y-direction L/R of each plane computed
+    // once per column pair of rows (two y-adjacent nodes share their window
+    // and, in line_lr2, their differences and quotients) by thread
+    // (t % TX, t / TX), one plane ahead of the pairs that use them.  Measured
+    // at 512^3: exact WENO5 23.11 -> 23.78 G, fast 57.9 -> 58.5 G; ENO3 (issue-
+    // bound, its y line is cheap) 83.4 -> 83.2 G, so ENO3 keeps the pair's own y.
+    constexpr bool YP = S >= WENO5;
     static_assert(NV == D + 1 && NB == 2 * W + D + 1, "ring geometry");
     extern __shared__ __align__(16) double sm[];
     const int n0 = P.n[0], n1 = P.n[1];
@@ -544,7 +559,10 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
     double* const ring = sm + (((128u - (smem_u32(sm) & 127u)) & 127u) >> 3);
     double* const vring = ring + NB * slot;
     double* const stage = vring + NV * M.vslot;
-    unsigned long long* const bar = reinterpret_cast<unsigned long long*>(stage + NS * M.hmax);
+    // YP: two (p, alpha*(R-L)) buffers of the y direction, one per plane parity
+    double2* const ybuf = reinterpret_cast<double2*>(stage + NS * M.hmax);
+    unsigned long long* const bar =
+        reinterpret_cast<unsigned long long*>(stage + NS * M.hmax + (YP ? 4 * TX * M.R : 0));
     const int t = threadIdx.x;
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
@@ -571,11 +589,35 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
     const bool generic_writes =
         border || (P.bc[2] != LSG_BC_PERIODIC && (P.z0 + zs - W < 0 || P.z0 + ze + W + D > nglob));
     const int nyh = 2 * W * cols, nh = nyh + 2 * W * rows;
+    // y-pass item: column yc, rows yr and yr+1 (the host picks even R with
+    // TX * R / 2 <= blockDim.x)
+    const int yc = t % TX, yr = 2 * (t / TX);
+    const bool yact = YP && yr < rows && yc < cols, ytwo = yact && yr + 1 < rows;
+    const int yoff = yr * pitch + yc + XL;  // slot row yr = tile row yr - W: the window's first value
+    const int yo = yr * TX + yc;
+    auto ypass = [&](const double* buf, double2* dst) {
+        if constexpr (YP) {
+            if (!yact) return;
+            double w[2 * W + 2];
+#pragma unroll
+            for (int k = 0; k < 2 * W + 2; ++k) w[k] = buf[yoff + k * pitch];
+            double La, Ra, Lb, Rb, p, term;
+            line_lr2<S>(w, P.lc[1], La, Ra, Lb, Rb);
+            costate_term<S>(P, 1, La, Ra, p, term);
+            dst[yo] = make_double2(p, term);
+            if (ytwo) {
+                costate_term<S>(P, 1, Lb, Rb, p, term);
+                dst[yo + TX] = make_double2(p, term);
+            }
+        }
+    };
 
 #ifdef LSG_CHECKED
     {
         unsigned dyn = 0;
         asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        LSG_CHECK(!YP || (M.R % 2 == 0 && TX * M.R <= 2 * (int)blockDim.x));
+        LSG_CHECK(!yact || yoff + (2 * W + 1) * pitch < slot);
         LSG_CHECK((smem_u32(ring) & 127u) == 0u);
         LSG_CHECK(reinterpret_cast<const char*>(bar + NB) <= reinterpret_cast<const char*>(sm) + dyn);
         LSG_CHECK(!active || (me + 1 + W * pitch < slot && vme + 1 < M.vslot));  // padding threads never read
@@ -728,6 +770,11 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
         }
     }
 
+    if constexpr (YP) {
+        __syncthreads();              // plane zs (slot W) fixed by every thread
+        ypass(ring + W * slot, ybuf);  // its y terms, read at z = zs
+    }
+
     unsigned long long kmin = ~0ull, kmax = 0ull;
     unsigned fz = ~0u;
     bool bad = false;
@@ -776,11 +823,17 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
             azn = __ldg(P.axis[2] + P.z0 + z + 1);
             trn = load_trig<KIND>(P, P.z0 + z + 1, 0);
         }
+        // y terms of plane z+1 (resident: z+1 <= z+W) into the other buffer; the
+        // pairs of plane z-1 read it before this iteration's barrier
+        const int yp = (z - zs) & 1;
+        if (YP && z + 1 < ze) {
+            const int j = j0 + W + 1;
+            ypass(ring + (j >= NB ? j - NB : j) * slot, ybuf + (yp ^ 1) * TX * M.R);
+        }
         if (active)
-            march3_pair<S, KIND, MODE, RANGE, S == ENO3>(P, zpl, me, pitch,
-                                                         MODE == MODE_COMBINE ? vring + vr * M.vslot + vme : nullptr,
-                                                         coli, z, two, ax0, ax1, ay, az, tr, kmin, kmax, fz, bad, &qa,
-                                                         &qb, z == zs);
+            march3_pair<S, KIND, MODE, RANGE, S == ENO3, YP>(
+                P, zpl, me, pitch, MODE == MODE_COMBINE ? vring + vr * M.vslot + vme : nullptr, coli, z, two, ax0,
+                ax1, ay, az, tr, kmin, kmax, fz, bad, &qa, &qb, z == zs, ybuf + yp * TX * M.R + vme);
         az = azn;
         tr = trn;
         j0 = j0 + 1 == NB ? 0 : j0 + 1;
