@@ -750,7 +750,8 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                         s->m3_hmax = 2 * Wr * (TX + R);
                         s->m3_smem = sizeof(double) * static_cast<size_t>(NB * s->m3_slot + NV * s->m3_vslot +
                                                                           (2 + 1) * s->m3_hmax +
-                                                                          (yp ? 4 * TX * R : 0)) +  // y-pass buffers
+                                                                          (yp ? 4 * TX * R : 0) +              // y-pass buffers
+                                                                          (kscheme == WENO5F ? 4 * threads : 0)) +  // z-pair slots
                                      sizeof(unsigned long long) * NB + 128;  // + alignment slack
                         for (int m = 0; m < 3; ++m)
                             for (int r = 0; r < 2; ++r)
@@ -1629,12 +1630,12 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
         CUDA_CHECK(cudaStreamCreateWithFlags(&s->cin, cudaStreamNonBlocking));
         CUDA_CHECK(cudaStreamCreateWithFlags(&s->cout, cudaStreamNonBlocking));
     }
-    while (static_cast<int>(s->pipe_ev.size()) < K + 2) {
+    while (static_cast<int>(s->pipe_ev.size()) < 2) {
         cudaEvent_t e;
         CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         s->pipe_ev.push_back(e);
     }
-    cudaEvent_t ev_start = s->pipe_ev[K], ev_done = s->pipe_ev[K + 1];
+    cudaEvent_t ev_start = s->pipe_ev[0], ev_done = s->pipe_ev[1];
     // level l reads u = ob[l-1], writes ob[l] (integrator.cpp:58-85 buffer use)
     const int a = s->cur;
     int ob[4] = {a, 0, 0, 0}, mode[4] = {0, MODE_EULER, MODE_COMBINE, MODE_COMBINE}, v0b[4] = {-1, -1, a, a};
@@ -1653,9 +1654,9 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
     const bool trace = std::getenv("LSG_PIPE_TRACE") != nullptr;
     std::vector<std::string> tnames;
     unsigned long long* tbuf = nullptr;
-    if (trace) CUDA_CHECK(cudaMallocAsync(&tbuf, 64 * sizeof(unsigned long long), ctx->stream));
+    if (trace) CUDA_CHECK(cudaMallocAsync(&tbuf, 128 * sizeof(unsigned long long), ctx->stream));
     auto mark = [&](const std::string& what, cudaStream_t st) {
-        if (!trace || tnames.size() >= 64) return;
+        if (!trace || tnames.size() >= 128) return;
         if (st != ctx->stream) {
             CUDA_CHECK(cudaEventRecord(ev_done, ctx->stream));  // tbuf allocated
             CUDA_CHECK(cudaStreamWaitEvent(st, ev_done, 0));
@@ -1664,13 +1665,25 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
         tnames.push_back(what);
     };
     mark("start", s->cin);
-    std::vector<int> cut(K + 1);
-    for (int j = 0; j <= K; ++j) cut[j] = static_cast<int>(static_cast<long long>(nz) * j / K);
-    for (int j = 0; j < K; ++j) {
-        CUDA_CHECK(cudaMemcpyAsync(sl.f[a] + cut[j] * plane, hin + cut[j] * plane,
-                                   sizeof(double) * static_cast<size_t>((cut[j + 1] - cut[j]) * plane),
+    // upload plan: K chunks of planes in order (ranges in upload order).
+    // Uploading a periodic axis's wrap planes first and tapering the last
+    // chunk measured equal (512^3: 24.05 vs 24.01 ms per step; the copy-in
+    // stream ends 0.8 ms before the step, so little is left to drain)
+    std::vector<std::pair<int, int>> up;
+    for (int j = 0; j < K; ++j)
+        up.emplace_back(static_cast<int>(static_cast<long long>(nz) * j / K),
+                        static_cast<int>(static_cast<long long>(nz) * (j + 1) / K));
+    const int nup = static_cast<int>(up.size());
+    while (static_cast<int>(s->pipe_ev.size()) < nup + 2) {
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s->pipe_ev.push_back(e);
+    }
+    for (int j = 0; j < nup; ++j) {
+        CUDA_CHECK(cudaMemcpyAsync(sl.f[a] + up[j].first * plane, hin + up[j].first * plane,
+                                   sizeof(double) * static_cast<size_t>((up[j].second - up[j].first) * plane),
                                    cudaMemcpyHostToDevice, s->cin));
-        CUDA_CHECK(cudaEventRecord(s->pipe_ev[j], s->cin));
+        CUDA_CHECK(cudaEventRecord(s->pipe_ev[2 + j], s->cin));
         mark("h2d chunk " + std::to_string(j), s->cin);
     }
     std::vector<std::vector<char>> done(S + 1, std::vector<char>(nz, 0));
@@ -1683,9 +1696,9 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
         }
         return true;
     };
-    for (int j = 0; j < K; ++j) {
-        for (int z = cut[j]; z < cut[j + 1]; ++z) done[0][z] = 1;
-        CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->pipe_ev[j], 0));
+    for (int j = 0; j < nup; ++j) {
+        for (int z = up[j].first; z < up[j].second; ++z) done[0][z] = 1;
+        CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->pipe_ev[2 + j], 0));
         std::vector<std::pair<int, int>> final_runs;
         for (int l = 1; l <= S; ++l) {
             for (int z = 0; z < nz;) {

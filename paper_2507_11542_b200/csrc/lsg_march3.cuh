@@ -156,12 +156,16 @@ __device__ __forceinline__ void eno3_z_step(double s6, const LineConst& c, Eno3Z
 // which fills them from the full window).
 // YP: the y-direction costates and dissipation terms of the pair come
 // precomputed (ypr[0], ypr[1]: (p, alpha*(R-L)) per node, the y pass of march3_tma_kernel).
-template <int S, int KIND, int MODE, bool RANGE, bool ZC = false, bool YP = false>
+// ZP: z lines two planes at a time: on zeven planes both nodes' z lines
+// cover planes z and z+1 (line_lr2 over zpl[0..2W+1]) and plane z+1's terms
+// go to zst[0..1]; on the other planes they come from there.
+template <int S, int KIND, int MODE, bool RANGE, bool ZC = false, bool YP = false, bool ZP = false>
 __device__ __forceinline__ void march3_pair(const StageParams& P, const double* const* zpl, int me, int pitch,
                                             const double* vpair, int coli, int z, bool two, double ax0, double ax1,
                                             double ay, double az, const Trig& tr, unsigned long long& kmin,
                                             unsigned long long& kmax, unsigned& fz, bool& bad, Eno3Z* qa = nullptr,
-                                            Eno3Z* qb = nullptr, bool first = true, const double2* ypr = nullptr) {
+                                            Eno3Z* qb = nullptr, bool first = true, const double2* ypr = nullptr,
+                                            double2* zst = nullptr, bool zeven = true) {
     constexpr int W = SchemeWidth<S>::W;
     using RS = RingShape<W>;
     constexpr int SH = RS::SH, XW = RS::XW;
@@ -215,6 +219,29 @@ __device__ __forceinline__ void march3_pair(const StageParams& P, const double* 
         costate<S>(P, 2, L, R, pa[2], da);
         eno3_z_step(v.y, P.lc[2], *qb, L, R);
         costate<S>(P, 2, L, R, pb[2], db);
+    } else if (ZP && zeven) {  // z: planes z and z+1 of both nodes
+        double wa[2 * W + 2], wb[2 * W + 2];
+#pragma unroll
+        for (int k = 0; k < 2 * W + 2; ++k) {
+            const double2 v = *reinterpret_cast<const double2*>(zpl[k]);
+            wa[k] = v.x;
+            wb[k] = v.y;
+        }
+        double L1, R1, p1, t1;
+        line_lr2<S>(wa, P.lc[2], L, R, L1, R1);
+        costate<S>(P, 2, L, R, pa[2], da);
+        costate_term<S>(P, 2, L1, R1, p1, t1);
+        zst[0] = make_double2(p1, t1);
+        line_lr2<S>(wb, P.lc[2], L, R, L1, R1);
+        costate<S>(P, 2, L, R, pb[2], db);
+        costate_term<S>(P, 2, L1, R1, p1, t1);
+        zst[1] = make_double2(p1, t1);
+    } else if (ZP) {
+        const double2 za = zst[0], zb = zst[1];
+        pa[2] = za.x;
+        da += za.y;
+        pb[2] = zb.x;
+        db += zb.y;
     } else {   // z: the pair's slot in the 2W+1 resident planes
         double wa[2 * W + 1], wb[2 * W + 1];
 #pragma unroll
@@ -549,6 +576,14 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
     // at 512^3: exact WENO5 23.11 -> 23.78 G, fast 57.9 -> 58.5 G; ENO3 (issue-
     // bound, its y line is cheap) 83.4 -> 83.2 G, so ENO3 keeps the pair's own y.
     constexpr bool YP = S >= WENO5;
+    // z pairs (fast WENO5): each pair's z lines two planes at a time
+    // (march3_pair ZP), waiting for plane z+W+1 on even planes of the chunk;
+    // the second plane's terms wait in a per-thread shared-memory slot.
+    // 512^3: fast 58.6 -> 59.6 G; the exact WENO5 spills with it (23.8 ->
+    // 22.7 G), so it keeps one z line per node and plane.  (A separate z pass
+    // before the pair's work, both planes' terms through shared memory, lost:
+    // fast 51.2 G, exact 22.4 G.)
+    constexpr bool ZP = S == WENO5F;
     static_assert(NV == D + 1 && NB == 2 * W + D + 1, "ring geometry");
     extern __shared__ __align__(16) double sm[];
     const int n0 = P.n[0], n1 = P.n[1];
@@ -561,8 +596,9 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
     double* const stage = vring + NV * M.vslot;
     // YP: two (p, alpha*(R-L)) buffers of the y direction, one per plane parity
     double2* const ybuf = reinterpret_cast<double2*>(stage + NS * M.hmax);
-    unsigned long long* const bar =
-        reinterpret_cast<unsigned long long*>(stage + NS * M.hmax + (YP ? 4 * TX * M.R : 0));
+    double2* const zst = ybuf + (YP ? 2 * TX * M.R : 0) + 2 * threadIdx.x;
+    unsigned long long* const bar = reinterpret_cast<unsigned long long*>(
+        stage + NS * M.hmax + (YP ? 4 * TX * M.R : 0) + (ZP ? 4 * (int)blockDim.x : 0));
     const int t = threadIdx.x;
     const int xt = blockIdx.x % M.ntx, yt = blockIdx.x / M.ntx;
     const int x0 = xt * TX, y0 = yt * M.R;
@@ -796,9 +832,22 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
 #pragma unroll 1
     for (int z = zs; z < ze; ++z) {
         const int jw = j0 + 2 * W >= NB ? j0 + 2 * W - NB : j0 + 2 * W;  // plane z+W
+        const bool zeven = ((z - zs) & 1) == 0;
         if (generic_writes) cp_async_wait<D - 1>();  // this thread's wrap copies of plane z+W
-        mbar_wait(bar + jw, (par >> jw) & 1u);
-        par ^= 1u << jw;
+        if (!ZP || zeven) {
+            mbar_wait(bar + jw, (par >> jw) & 1u);
+            par ^= 1u << jw;
+        }
+        // plane z+W+1 for the z lines of plane z+1 (own cells only: no fix-up
+        // needed).  An odd chunk's last plane has no plane z+1: node b of its
+        // z lines reads a stale slot, and node a's bits do not depend on it
+        // (line_lr2: a's window is s[0..2W]; an operand outside the fast
+        // divisions' domain only sends both to the IEEE path)
+        if (ZP && zeven && z + 1 < ze) {
+            const int jn = jw + 1 == NB ? 0 : jw + 1;
+            mbar_wait(bar + jn, (par >> jn) & 1u);
+            par ^= 1u << jn;
+        }
         fixup(z + W, jw, sr);
         // generic-proxy writes of the ring (fix-ups, extrapolated planes) before
         // the TMA writes that will reuse their slots (issued after the barrier)
@@ -811,9 +860,9 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
             issue(z + W + D, ji, vi, si);
             if (generic_writes) cp_async_commit();
         }
-        const double* zpl[2 * W + 1];
+        const double* zpl[2 * W + 2];
 #pragma unroll
-        for (int k = 0; k < 2 * W + 1; ++k) {
+        for (int k = 0; k < 2 * W + 2; ++k) {
             const int j = j0 + k;
             zpl[k] = ring + (j >= NB ? j - NB : j) * slot + me;
         }
@@ -831,9 +880,9 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
             ypass(ring + (j >= NB ? j - NB : j) * slot, ybuf + (yp ^ 1) * TX * M.R);
         }
         if (active)
-            march3_pair<S, KIND, MODE, RANGE, S == ENO3, YP>(
+            march3_pair<S, KIND, MODE, RANGE, S == ENO3, YP, ZP>(
                 P, zpl, me, pitch, MODE == MODE_COMBINE ? vring + vr * M.vslot + vme : nullptr, coli, z, two, ax0,
-                ax1, ay, az, tr, kmin, kmax, fz, bad, &qa, &qb, z == zs, ybuf + yp * TX * M.R + vme);
+                ax1, ay, az, tr, kmin, kmax, fz, bad, &qa, &qb, z == zs, ybuf + yp * TX * M.R + vme, zst, zeven);
         az = azn;
         tr = trn;
         j0 = j0 + 1 == NB ? 0 : j0 + 1;

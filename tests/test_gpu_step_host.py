@@ -27,6 +27,7 @@ def cases():
         "cfg1_41": (P.CONFIGS["cfg1"](n=41), None),                # 2-D, clamped (extrapolated) slab axis
         "cfg3_29": (P.cfg3_dblint4(29), None),                     # 4-D WENO5
         "cfg5_32": (P.cfg5_normal(32), None),                      # periodic box WENO5
+        "cfg5_32x120": (P.cfg5_normal(32, nz=120), None),          # wrap planes first, tapered last chunk
         "rockets_30": (P.rockets(30), None),                       # non-periodic heading
         "lin6_40": (dataclasses.replace(P.cfg1_circle(21), grid=g6, problem=lin6, method=abi.CFL3), "random"),
         "cfg2_21_fallback": (P.cfg2_air3d(21), None),              # 21 planes: too few to pipeline
