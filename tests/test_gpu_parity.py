@@ -320,6 +320,38 @@ def test_march3_tilings_vs_oracle(ctx, port, counts, periodic):
         assert_bitwise(va, vb, f"v scheme {s}")
 
 
+@pytest.mark.parametrize("counts,periodic", [
+    ((300, 20, 9), (0, 1, 2)),     # TMA tiles 32x16, chunks of odd and even length
+    ((160, 9, 8), (0,)),           # full rows of 160: R = 3 made even for the y pass
+    ((250, 11, 7), (2,)),          # ragged last segment
+    ((64, 64, 37), (0, 1, 2)),     # z chunks of 5 planes (below): the z pairs' odd last plane
+    ((101, 21, 13), ()),           # odd rows: the cp.async tile kernel
+])
+def test_march3_tilings_fast_weno5_matches_generic(ctx, monkeypatch, counts, periodic):
+    """The fast WENO5 on the tile kernels (y pass, z pairs) against the
+    one-node-per-thread kernel: the same per-node arithmetic, so the same bits
+    (a few RK3 steps)."""
+    g = abi.make_grid([-1.0, 0.0, 2.0], [1.0, 3.0, 5.0], list(counts), periodic)
+    v = H.random_field(g, sum(counts) + 1)
+    p = abi.make_problem(abi.HAM_LINEAR, abi.SCHEME_WENO5, abi.linear_params([0.7, -1.1, 0.4]), abi.GROW, False,
+                         options=abi.OPT_WENO5_FAST)
+    out = []
+    if counts[2] == 37:
+        monkeypatch.setenv("LSG_M3_CHUNK", "5")
+    for kernel in (None, "generic"):
+        if kernel:
+            monkeypatch.setenv("LSG_KERNEL", kernel)
+        s = _lib.Solver(ctx, g, p, abi.CFL3)
+        s.set_field(v)
+        dt = 0.32 * s.step_bound()
+        log, _ = s.integrate(0.0, 3 * dt)
+        out.append((np.asarray(log), s.get_field()))
+        s.close()
+    assert len(out[0][0]) >= 2
+    assert_bitwise(out[0][0], out[1][0], "step log, tiles vs generic")
+    assert_bitwise(out[0][1], out[1][1], "v, tiles vs generic")
+
+
 def test_generic_kernel_3d_still_exact(ctx, port, monkeypatch):
     """LSG_KERNEL=generic forces the one-thread-per-node kernel on 3-D grids."""
     monkeypatch.setenv("LSG_KERNEL", "generic")
