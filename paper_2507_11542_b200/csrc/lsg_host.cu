@@ -1696,10 +1696,13 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
         }
         return true;
     };
+    // finished runs go back after every compute round, adjacent runs as one
+    // copy (holding them back for larger copies measured slower: 512^3, 64 /
+    // 128 / 256 MiB batches 25.9 / 26.6 / 28.3 ms per step against 24.2)
+    std::vector<std::pair<int, int>> final_runs;
     for (int j = 0; j < nup; ++j) {
         for (int z = up[j].first; z < up[j].second; ++z) done[0][z] = 1;
         CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, s->pipe_ev[2 + j], 0));
-        std::vector<std::pair<int, int>> final_runs;
         for (int l = 1; l <= S; ++l) {
             for (int z = 0; z < nz;) {
                 if (done[l][z] || !ready(l, z)) {
@@ -1711,7 +1714,10 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
                 launch_planes(s, sl, mode[l], ob[l - 1], v0b[l], ob[l], dt, cw[l], l == S ? range : nullptr, z, e, 0,
                               0, ctx->stream);
                 for (int q = z; q < e; ++q) done[l][q] = 1;
-                if (l == S) final_runs.emplace_back(z, e);
+                if (l == S) {
+                    if (!final_runs.empty() && final_runs.back().second == z) final_runs.back().second = e;
+                    else final_runs.emplace_back(z, e);
+                }
                 z = e;
             }
         }
@@ -1724,6 +1730,7 @@ void step_host_pipelined(lsg_solver* s, double dt, const double* hin, double* ho
                                            sizeof(double) * static_cast<size_t>((r.second - r.first) * plane),
                                            cudaMemcpyDeviceToHost, s->cout));
             mark("d2h after round " + std::to_string(j), s->cout);
+            final_runs.clear();
         }
     }
     for (int z = 0; z < nz; ++z)
