@@ -11,9 +11,11 @@ int main() {
     cudaMallocHost(&h2, n);
     cudaMalloc(&d1, n);
     cudaMalloc(&d2, n);
-    cudaStream_t a, b;
+    cudaStream_t a, b, a2, b2;
     cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&b, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&a2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&b2, cudaStreamNonBlocking);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -22,19 +24,20 @@ int main() {
         for (int rep = 0; rep < 3; ++rep) {
             cudaDeviceSynchronize();
             cudaEventRecord(e0, 0);
-            cudaStreamWaitEvent(a, e0, 0);
-            cudaStreamWaitEvent(b, e0, 0);
-            for (size_t o = 0; o < n; o += c) {
-                if (mode & 1) cudaMemcpyAsync((char*)d1 + o, (char*)h1 + o, c, cudaMemcpyHostToDevice, a);
-                if (mode & 2) cudaMemcpyAsync((char*)h2 + o, (char*)d2 + o, c, cudaMemcpyDeviceToHost, b);
+            for (cudaStream_t st : {a, b, a2, b2}) cudaStreamWaitEvent(st, e0, 0);
+            const bool two = mode & 4;  // alternate chunks over two streams per direction
+            size_t k = 0;
+            for (size_t o = 0; o < n; o += c, ++k) {
+                cudaStream_t sa = two && (k & 1) ? a2 : a, sb = two && (k & 1) ? b2 : b;
+                if (mode & 1) cudaMemcpyAsync((char*)d1 + o, (char*)h1 + o, c, cudaMemcpyHostToDevice, sa);
+                if (mode & 2) cudaMemcpyAsync((char*)h2 + o, (char*)d2 + o, c, cudaMemcpyDeviceToHost, sb);
             }
-            cudaEvent_t ea, eb;
-            cudaEventCreate(&ea);
-            cudaEventCreate(&eb);
-            cudaEventRecord(ea, a);
-            cudaEventRecord(eb, b);
-            cudaStreamWaitEvent(0, ea, 0);
-            cudaStreamWaitEvent(0, eb, 0);
+            for (cudaStream_t st : {a, b, a2, b2}) {
+                cudaEvent_t ev;
+                cudaEventCreate(&ev);
+                cudaEventRecord(ev, st);
+                cudaStreamWaitEvent(0, ev, 0);
+            }
             cudaEventRecord(e1, 0);
             cudaEventSynchronize(e1);
             float ms;
@@ -48,5 +51,9 @@ int main() {
     run("D2H 1 GiB", 2, n);
     run("H2D + D2H concurrent", 3, n);
     run("H2D + D2H, 32 MiB chunks", 3, chunk);
+    run("H2D, 2 streams, 32 MiB", 5, chunk);
+    run("D2H, 2 streams, 32 MiB", 6, chunk);
+    run("H2D + D2H, 2+2 streams", 7, chunk);
+    run("H2D 32 MiB chunks", 1, chunk);
     return 0;
 }
