@@ -72,6 +72,7 @@ __device__ double draw(unsigned long long h, int mode) {
         case 2: return ldexp(u * 2.0 - 1.0, (int)((h >> 3) % 200) - 100);      // mixed magnitudes
         case 3: return ldexp(u, -1000 - (int)(h % 60));                          // subnormal-adjacent differences
         case 4: return ldexp(u * 2.0 - 1.0, 900 + (int)(h % 120));              // huge (and overflowing) values
+        case 6: return ldexp(u * 2.0 - 1.0, ((h >> 7) & 1 ? -262 : 238) + (int)((h >> 3) % 16));  // edges of the fast path's range
         default: return (h & 1) ? 0.0 : -0.0;                                    // signed zeros
     }
 }
@@ -84,7 +85,7 @@ __global__ void check_lr(unsigned long long seed, long long n, LineConst c) {
         double s[8];
         for (int j = 0; j < 8; ++j) {
             const unsigned long long h = mix(h0 + 0x51ull * (j + 1));
-            s[j] = draw(h, mode < 6 ? 0 : mode < 9 ? 1 : mode < 12 ? 2 : mode < 13 ? 3 : mode < 14 ? 4 : mode < 15 ? 5 : (int)(h % 6));
+            s[j] = draw(h, mode < 5 ? 0 : mode < 8 ? 1 : mode < 11 ? 2 : mode < 12 ? 3 : mode < 13 ? 4 : mode < 14 ? 5 : mode < 15 ? 6 : (int)(h % 7));
             if (mode == 7 && j > 0 && (h & 3) == 0) s[j] = s[j - 1];  // flat runs
         }
         // reference: plain IEEE divisions in the reference's order
