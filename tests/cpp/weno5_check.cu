@@ -55,7 +55,14 @@ __global__ void check_div(unsigned long long seed, long long n) {
         if (i == 4) x = __longlong_as_double(0x7E6FFFFFFFFFFFFFll);  // largest admitted
         if (i == 5) x = 3.0;
         if (i == 6) x = -6.0;
-        if (!weno5_operand_ok(x)) report(1, x);
+        if (i == 7) x = 0x1p-250;
+        if (i == 8) x = -0x1.fffffffffffffp+249;  // largest the fast path admits
+        if (i == 9) x = 0x1p250;                  // smallest it refuses above
+        if (i == 10) x = 0x1.fffffffffffffp-251;  // largest it refuses below
+        // the fast path's operand test admits exactly +-0 and 2^-250 <= |x| < 2^250
+        // (a subset of the range checked for the divisions here)
+        const double ax = fabs(x);
+        if (weno5_operand_ok(x) != (ax == 0.0 || (ax >= 0x1p-250 && ax < 0x1p250))) report(1, x);
         if (!same(div_by3(x), x / 3.0) || !same(div_by6(x), x / 6.0)) report(2, x);
         if (!same(0.5 * div_by3(x), x / 6.0)) report(3, x);
         ++cnt;
