@@ -681,6 +681,9 @@ def b200_arm(args):
         "e2e_leg": e2e_leg,
         "clocks": sampler.summary(),
     }
+    if e2e is None and not args.no_e2e:
+        line["e2e_note"] = (f"not measured: the per-step host round trip of a {8 * nodes_local / 1e9:.1f} GB field "
+                            "needs that much pinned host memory twice over (measured up to 8 GiB fields)")
     if extras:
         line["extras"] = extras
     if eff:
