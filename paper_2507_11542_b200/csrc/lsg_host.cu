@@ -748,11 +748,13 @@ std::unique_ptr<lsg_solver> make_solver(lsg_ctx* ctx, const lsg_grid* g, const l
                         s->m3_slot = ((s->m3_pitch * rows_box + 15) / 16) * 16;
                         s->m3_vslot = ((TX * R + 15) / 16) * 16;
                         s->m3_hmax = 2 * Wr * (TX + R);
-                        s->m3_smem = sizeof(double) * static_cast<size_t>(NB * s->m3_slot + NV * s->m3_vslot +
-                                                                          (2 + 1) * s->m3_hmax +
+                        // ring depth of march3_tma_kernel (TmaDepth in lsg_march3.cuh): planes in flight
+                        const int Dt = kscheme == WENO5 ? 1 : 2, NBt = 2 * Wr + 1 + Dt, NVt = Dt + 1;
+                        s->m3_smem = sizeof(double) * static_cast<size_t>(NBt * s->m3_slot + NVt * s->m3_vslot +
+                                                                          (Dt + 1) * s->m3_hmax +
                                                                           (yp ? 4 * TX * R : 0) +              // y-pass buffers
                                                                           (kscheme == WENO5F ? 4 * threads : 0)) +  // z-pair slots
-                                     sizeof(unsigned long long) * NB + 128;  // + alignment slack
+                                     sizeof(unsigned long long) * NBt + 128;  // + alignment slack
                         for (int m = 0; m < 3; ++m)
                             for (int r = 0; r < 2; ++r)
                                 CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(s->m3tfn[m][r]),

@@ -528,6 +528,14 @@ using March3Fn = void (*)(StageParams, March3);
 // edge are extrapolated by the threads as in march3_kernel.  Needs rows of an
 // even number of doubles (16-byte global strides); other grids use
 // march3_kernel.
+// Planes in flight of the TMA ring (the host sizes shared memory to match).
+// The exact WENO5 spends ~5 us per plane, so one plane in flight hides the
+// load (25.03 -> 25.09 G at 512^3) and frees 11 KB of shared memory.
+template <int S>
+struct TmaDepth {
+    static constexpr int D = S == WENO5 ? 1 : 2;
+};
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -566,7 +574,7 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
                       const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmv) {
     constexpr int W = SchemeWidth<S>::W;
     using RS = RingShape<W>;
-    constexpr int D = RS::D, NB = RS::NB, NV = RS::NV, SH = RS::SH;
+    constexpr int D = TmaDepth<S>::D, NB = 2 * W + 1 + D, NV = D + 1, SH = RS::SH;
     constexpr int XL = W + SH;  // box columns start XL left of the tile
     constexpr int NS = D + 1;   // staging slots (planes whose wrap cells are in flight)
     // y pass (WENO5, both forms): the y-direction L/R of each plane computed
@@ -584,7 +592,7 @@ __global__ void __launch_bounds__(256, S <= ENO2 ? 3 : 2)
     // before the pair's work, both planes' terms through shared memory, lost:
     // fast 51.2 G, exact 22.4 G.)
     constexpr bool ZP = S == WENO5F;
-    static_assert(NV == D + 1 && NB == 2 * W + D + 1, "ring geometry");
+    static_assert(NV == D + 1 && NB == 2 * W + D + 1 && NB <= 32, "ring geometry");
     extern __shared__ __align__(16) double sm[];
     const int n0 = P.n[0], n1 = P.n[1];
     const long long s2 = P.stride[2];
