@@ -60,6 +60,28 @@ __device__ __forceinline__ void block_range(unsigned long long* slot, unsigned l
     }
 }
 
+// One node's line as an out-of-line call: the 6-D exact-WENO5 kernel calls it
+// once per dimension, so one copy of the scheme's code serves all six
+// (unrolled, they overflow the instruction cache) while the dimension loop
+// stays unrolled (p[] in registers).  Measured (41^6 / 81^4): exact WENO5
+// 9.40 -> 9.63 G in 6-D, but 15.64 -> 15.10 G in 4-D; the fast WENO5 (18.7 ->
+// 17.4 G) and ENO3 (21.8 -> 19.1 G) lose in 6-D, so exact WENO5 in 6-D only.
+struct LRv {
+    double L, R;
+};
+template <int S>
+static __device__ __noinline__ LRv line_call(double s0, double s1, double s2, double s3, double s4, double s5,
+                                             double s6, LineConst c) {
+    const double s[7] = {s0, s1, s2, s3, s4, s5, s6};
+    LRv r;
+    line_lr<S>(s, c, r.L, r.R);
+    return r;
+}
+template <int S, int D>
+struct OutOfLineLine {
+    static constexpr bool value = D >= 6 && S == WENO5;
+};
+
 // One node of a fused stage (hamiltonian.cpp:11-88 + integrator.cpp:58-85):
 // L/R per dimension, central costate, H, global-LF dissipation, clamp, and
 // the TVD-RK combination of MODE.  Returns the stage output at idx.
@@ -91,7 +113,13 @@ __device__ __forceinline__ double stage_node(const StageParams& P, const double*
         gather_window<W>(u, idx, i[d], P.n[d], P.stride[d], P.bc[d], d == D - 1, P.z0, P.nz_glob, P.halo, s,
                          -(long long)P.halo * W * P.plane, P.n_local + (long long)P.halo * W * P.plane);
         double L, R;
-        line_lr<S>(s, P.lc[d], L, R);
+        if constexpr (OutOfLineLine<S, D>::value) {
+            const LRv r = line_call<S>(s[0], s[1], s[2], s[3], s[4], s[5], s[6], P.lc[d]);
+            L = r.L;
+            R = r.R;
+        } else {
+            line_lr<S>(s, P.lc[d], L, R);
+        }
         costate<S>(P, d, L, R, p[d], diss);  // hamiltonian.cpp:31-32, 60-64
     }
     const double H = hamiltonian<KIND, D>(P, x, load_trig<KIND>(P, D > 2 ? ix[D > 2 ? 2 : 0] : 0, D > 5 ? ix[D > 5 ? 5 : 0] : 0), p);
